@@ -1,0 +1,211 @@
+"""Generate golden vectors from the REFERENCE implementation (build container only).
+
+Runs /root/reference/pkg/src/densify360 (numba) on small synthetic scenes and stores
+inputs + outputs of every hot-path function under tests/golden/*.npz.  The reference
+cannot travel to the GPU box, these fixtures can.  Re-run:
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache python oracle/gen_golden.py
+
+Nothing under tests/, bench.py or the package reads /root/reference at run time.
+"""
+import os
+import sys
+from pathlib import Path
+
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+os.environ.setdefault("NUMBA_NUM_THREADS", "8")
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, "/root/reference/pkg/tests")
+
+import numpy as np
+
+from densify360 import engine, kernels, pipeline  # noqa: E402
+from densify360.engine import PatchSpec, PlaneMap  # noqa: E402
+from densify360.geometry import EquirectCamera, RigidPose, camera_rays  # noqa: E402
+from densify360.keyframes import Keyframe, StereoGroup, to_gray  # noqa: E402
+from densify360.synth import default_scene, render_scene  # noqa: E402
+
+OUT = Path(__file__).resolve().parent.parent / "tests" / "golden"
+OUT.mkdir(parents=True, exist_ok=True)
+DEPTH_RANGE = (0.5, 16.0)
+
+
+def rot(axis, deg):
+    a = np.radians(deg)
+    c, s = np.cos(a), np.sin(a)
+    m = {0: [[1, 0, 0], [0, c, -s], [0, s, c]], 1: [[c, 0, s], [0, 1, 0], [-s, 0, c]],
+         2: [[c, -s, 0], [s, c, 0], [0, 0, 1]]}[axis]
+    return np.array(m, np.float64)
+
+
+def make_frames(cam, poses, scene_kind="box"):
+    scene = default_scene(scene_kind)
+    frames, gts = [], []
+    for k, pose in enumerate(poses):
+        image, pano = render_scene(scene, cam, pose)
+        frames.append(Keyframe(id=k, image=image, pose=pose))
+        gts.append(pano.depth)
+    return frames, gts
+
+
+def pose_arrays(frames):
+    return (np.stack([f.pose.rotation for f in frames]),
+            np.stack([f.pose.translation for f in frames]))
+
+
+def hot_path_case(name, width, iterations, poses, spec, seed, full_trace):
+    """eval → (red, black, refine)*I with the state after every pass."""
+    cam = EquirectCamera(width, width // 2)
+    frames, gts = make_frames(cam, poses)
+    group = StereoGroup(reference=frames[1], neighbors=(frames[0], frames[2]), camera=cam)
+    prep = engine.prepare_group(group, spec)
+    init = engine.random_init(PlaneMap.empty(cam, DEPTH_RANGE), DEPTH_RANGE, seed=seed)
+    rng = np.random.default_rng(seed)
+    tables = engine._refinement_draw_tables(
+        rng, iterations, engine.DEFAULT_REFINE_DEPTH_FRACTION * (DEPTH_RANGE[1] - DEPTH_RANGE[0]),
+        np.radians(engine.DEFAULT_REFINE_THETA_DEG))
+    trunc = spec.cost_truncation
+    out = {
+        "images": np.stack([f.image for f in frames]),
+        "rotations": pose_arrays(frames)[0], "translations": pose_arrays(frames)[1],
+        "gt_depth": gts[1].astype(np.float32),
+        "half_window": spec.half_window, "sample_stride": spec.sample_stride, "trunc": trunc,
+        "depth_range": np.array(DEPTH_RANGE), "seed": seed, "iterations": iterations,
+        "init_depth": init.depth, "init_normal": init.normal,
+        "ref_gray": prep.ref_gray, "rays": prep.rays, "rel_r": prep.rel_r, "rel_t": prep.rel_t,
+        "offsets": prep.offsets,
+        "tables": np.stack([np.stack(t) for t in tables]),
+    }
+    cur = init.copy()
+    engine._evaluate_all(prep, cur.depth, cur.normal, cur.cost)
+    steps = [("eval", cur.copy())]
+    nxt = cur.copy()
+    for it in range(iterations):
+        for parity in (0, 1):
+            np.copyto(nxt.depth, cur.depth); np.copyto(nxt.normal, cur.normal); np.copyto(nxt.cost, cur.cost)
+            kernels.red_black_pass(parity, kernels.NEIGHBOR_OFFSETS, cur.depth, cur.normal, cur.cost,
+                                   nxt.depth, nxt.normal, nxt.cost, prep.rays, prep.ref_gray,
+                                   prep.nb0, prep.nb1, prep.rel_r, prep.rel_t, prep.offsets, trunc)
+            cur, nxt = nxt, cur
+            steps.append((f"rb{it}.{parity}", cur.copy()))
+        dd, sa, ca, caz, saz = tables[it]
+        kernels.refine_pass(cur.depth, cur.normal, cur.cost, dd, sa, ca, caz, saz, DEPTH_RANGE[0],
+                            DEPTH_RANGE[1], prep.rays, prep.ref_gray, prep.nb0, prep.nb1, prep.rel_r,
+                            prep.rel_t, prep.offsets, trunc)
+        steps.append((f"refine{it}", cur.copy()))
+    # cross-check against the reference's own driver
+    pm, pano = engine.run_patchmatch(group, init, spec, iterations=iterations, seed=seed, workers=8)
+    assert np.array_equal(pm.depth, cur.depth) and np.array_equal(pm.cost, cur.cost)
+    keep = steps if full_trace else [steps[0], steps[1], steps[2], steps[3], steps[-1]]
+    out["step_names"] = np.array([s[0] for s in keep])
+    out["step_depth"] = np.stack([s[1].depth for s in keep])
+    out["step_normal"] = np.stack([s[1].normal for s in keep])
+    out["step_cost"] = np.stack([s[1].cost for s in keep])
+    out["pano_valid"] = pano.valid
+    med = engine.median_outlier_filter(pano, window=5, rel_threshold=0.2)
+    out["median_valid"] = med.valid
+    # float64 reference cost (E:169-224) at a few pixels of the final map
+    from densify360.geometry import PlaneHypothesis
+    pr = np.random.default_rng(1)
+    px = np.stack([pr.integers(0, cam.width, 40), pr.integers(0, cam.height, 40)], 1)
+    pc = []
+    for x, y in px:
+        n = init.normal[y, x].astype(np.float64)
+        n /= np.linalg.norm(n)
+        pc.append(engine.patch_cost(prep, (x, y), PlaneHypothesis(float(init.depth[y, x]), n), spec))
+    out["patch_cost_px"] = px
+    out["patch_cost"] = np.array(pc)
+    np.savez_compressed(OUT / f"{name}.npz", **out)
+    print(name, "steps", len(keep), "final mean cost", float(cur.cost.mean()), "valid", float(pano.valid.mean()))
+
+
+def stage_case():
+    """DepthStage chain (warp + random init), consistency filter, fusion on 64x32."""
+    cam = EquirectCamera(64, 32)
+    spec = PatchSpec()
+    n_kf = 9
+    poses = [RigidPose(rotation=rot(1, 2.0 * k) @ rot(0, 1.0 * k),
+                       translation=np.array([0.02 * k, 0.01 * k, -0.6 + 0.15 * k])) for k in range(n_kf)]
+    frames, gts = make_frames(cam, poses)
+    stage = pipeline.DepthStage(cam, spec, DEPTH_RANGE, iterations=2, seed=3, warp=True, workers=8)
+    results = []
+    warp_io = None
+    for k in range(1, n_kf - 1):
+        group = StereoGroup(reference=frames[k], neighbors=(frames[k - 1], frames[k + 1]), camera=cam)
+        if k == 2:
+            prev_map, prev_pose = stage._prev
+            w = engine.warp_plane_map(prev_map, prev_pose, frames[k].pose, cam)
+            warp_io = (prev_map.copy(), w)
+        results.append(stage.process(group))
+    out = {
+        "images": np.stack([f.image for f in frames]),
+        "rotations": pose_arrays(frames)[0], "translations": pose_arrays(frames)[1],
+        "depth_range": np.array(DEPTH_RANGE), "seed": 3, "iterations": 2,
+        "stage_ids": np.array([r.id for r in results]),
+        "stage_depth": np.stack([r.pano.depth for r in results]),
+        "stage_valid": np.stack([r.pano.valid for r in results]),
+        "warp_src_depth": warp_io[0].depth, "warp_src_normal": warp_io[0].normal,
+        "warp_src_cost": warp_io[0].cost, "warp_src_valid": warp_io[0].valid,
+        "warp_out_depth": warp_io[1].depth, "warp_out_normal": warp_io[1].normal,
+        "warp_out_cost": warp_io[1].cost, "warp_out_valid": warp_io[1].valid,
+    }
+    # consistency + fusion on ground-truth panoramas with a sprinkling of outliers
+    rng = np.random.default_rng(5)
+    panos = []
+    for k in range(5):
+        d = gts[k + 1].astype(np.float32).copy()
+        v = rng.uniform(size=d.shape) > 0.1
+        bad = rng.uniform(size=d.shape) < 0.2
+        d[bad] *= rng.uniform(0.7, 1.3, size=int(bad.sum())).astype(np.float32)
+        panos.append(engine.DepthPanorama(cam, d, v))
+    ccfg = pipeline.ConsistencyConfig()
+    target = panos[2]
+    others = [(panos[i], poses[i + 1]) for i in (0, 1, 3, 4)]
+    filt = pipeline.consistency_filter(target, poses[3], others, ccfg)
+    out.update(cons_depth=np.stack([p.depth for p in panos]), cons_valid=np.stack([p.valid for p in panos]),
+               cons_out_valid=filt.valid)
+    fcfg = pipeline.FusionConfig()
+    fb = pipeline.FusionBuffer(cam, fcfg)
+    cloud = None
+    for k in range(4):
+        res = pipeline.DepthResult(id=k + 1, pano=panos[k], pose=poses[k + 1], image=frames[k + 1].image, seconds=0.0)
+        got = fb.push(res)
+        if got is not None:
+            cloud = got
+    out.update(fuse_points=cloud.points, fuse_colors=cloud.colors, fuse_ids=cloud.source_ids)
+    np.savez_compressed(OUT / "stage_64x32.npz", **out)
+    print("stage", [float(r.pano.valid.mean()) for r in results], "warp fill", float(warp_io[1].valid.mean()),
+          "cons survive", float(filt.valid.mean()), "fused", len(cloud.points))
+
+
+def misc_case():
+    """random_init known answers (PCG64), to_gray, rays, median edge cases."""
+    cam = EquirectCamera(32, 16)
+    pm = PlaneMap.empty(cam, (0.5, 8.0))
+    pm.depth[3, 7] = 2.25
+    pm.normal[3, 7] = (0, 0, -1)
+    pm.valid[3, 7] = True
+    ri = engine.random_init(pm, (0.5, 8.0), seed=42)
+    rng = np.random.default_rng(9)
+    img = rng.integers(0, 256, size=(16, 32, 3), dtype=np.uint8)
+    depth = rng.uniform(0.5, 8.0, size=(16, 32)).astype(np.float32)
+    valid = rng.uniform(size=(16, 32)) > 0.3
+    med3 = engine.median_outlier_filter(engine.DepthPanorama(cam, depth, valid), 3, 0.2).valid
+    med7 = engine.median_outlier_filter(engine.DepthPanorama(cam, depth, valid), 7, 0.35).valid
+    np.savez_compressed(OUT / "misc_32x16.npz", ri_depth=ri.depth, ri_normal=ri.normal, ri_cost=ri.cost,
+                        ri_valid=ri.valid, gray_in=img, gray_out=to_gray(img), gray2_out=to_gray(img[..., 0]),
+                        rays32=camera_rays(cam).astype(np.float32), med_depth=depth, med_valid=valid,
+                        med3=med3, med7=med7)
+    print("misc ok")
+
+
+if __name__ == "__main__":
+    ident = lambda z: RigidPose(rotation=np.eye(3), translation=np.array([0.0, 0.0, z]))
+    hot_path_case("hot_64x32_ident", 64, 3, [ident(-0.15), ident(0.0), ident(0.15)], PatchSpec(), 7, True)
+    rposes = [RigidPose(rot(1, -7.0) @ rot(0, 3.0), np.array([0.05, -0.02, -0.17])),
+              RigidPose(rot(2, 4.0), np.array([0.0, 0.0, 0.0])),
+              RigidPose(rot(1, 9.0) @ rot(2, -5.0), np.array([-0.04, 0.03, 0.16]))]
+    hot_path_case("hot_64x32_rot", 64, 2, rposes, PatchSpec(half_window=3, sample_stride=1), 11, True)
+    hot_path_case("hot_256x128_c1", 256, 3, [ident(-0.15), ident(0.0), ident(0.15)], PatchSpec(), 0, False)
+    stage_case()
+    misc_case()
