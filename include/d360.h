@@ -1,0 +1,174 @@
+/*
+ * d360.h — C ABI of the B200-native densify360 hot path (libd360.so).
+ *
+ * The reference has no FFI: its operator boundary is the Python module
+ * densify360.kernels (four numba functions over C-contiguous arrays), called only by
+ * densify360.engine, plus two numpy routines in densify360.pipeline.  Every entry point
+ * below replaces one of those call targets; "replaces" cites the reference file:line
+ * (K = pkg/src/densify360/kernels.py, E = engine.py, P = pipeline.py, G = geometry.py,
+ * KF = keyframes.py, SY = synth.py).
+ *
+ * Conventions
+ *  - plain pointers and sizes only; no torch / numpy types.
+ *  - pointers documented "device" are CUDA device pointers owned by the caller;
+ *    "host" pointers are small parameter blocks read before the call returns.
+ *  - `stream` is a cudaStream_t passed as void*; calls are asynchronous on it unless
+ *    stated otherwise.  The library allocates nothing persistent.
+ *  - return 0 on success, nonzero on error; d360_last_error() describes the failure
+ *    (thread-local).  Kernels never "raise": unusable hypotheses score `trunc`
+ *    exactly as the reference does (K:32-37).
+ *  - images / state use the reference's array layouts: depth (H,W) f32, normal (H,W,3)
+ *    f32, cost (H,W) f32, masks (H,W) u8 (numpy bool), rays (H,W,3) f32.
+ */
+#ifndef D360_H
+#define D360_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define D360_MAX_VIEWS 8
+#define D360_MAX_SAMPLES 128
+#define D360_MAX_REACH 8      /* max |dx|,|dy| of a patch sample offset */
+#define D360_MAX_REFINE 16    /* max refinement candidates per pass (reference: 6) */
+#define D360_MAX_FRAMES 8     /* max frames in a consistency window / fusion buffer */
+
+/* Arithmetic policy of the cost kernels. */
+enum {
+    D360_PREC_EXACT = 0, /* literal f64 restatement (IEEE div/sqrt, f64 bilinear + sums) */
+    D360_PREC_MIXED = 1, /* f64 projection with Newton-refined rcp/rsqrt, f32 bilinear  */
+    D360_PREC_FAST = 2   /* reserved: all-f32 projection                                */
+};
+
+/* One stereo group in kernel layout == densify360.engine.PreparedGroup (E:137-156),
+ * generalised from 2 to n_views neighbours. */
+typedef struct d360_group {
+    int32_t width, height;      /* W == 2H (G:40) */
+    int32_t n_views;            /* 1..D360_MAX_VIEWS */
+    int32_t n_samples;          /* 1..D360_MAX_SAMPLES */
+    int32_t top_k;              /* 1..n_views; cost = mean of the k smallest per-view costs.
+                                   n_views=2, top_k=2 is the reference's 0.5*(c0+c1) (K:297) */
+    int32_t precision;          /* D360_PREC_* */
+    const float *rays;          /* device (H,W,3) */
+    const float *ref_gray;      /* device (H,W) */
+    const float *nb;            /* device (V,H,W) neighbour luma */
+    const float *rel_r;         /* host (V,3,3) x_nb = R x_ref + t (G:182-188), f32 (E:152) */
+    const float *rel_t;         /* host (V,3) */
+    const int32_t *offsets;     /* host (S,2) as (dx,dy) (E:60-65) */
+    double trunc;               /* PatchSpec.cost_truncation */
+} d360_group;
+
+const char *d360_last_error(void);
+int d360_version(void);
+
+/* replaces kernels.eval_costs (K:300-349; caller E:366-379) */
+int d360_eval_costs(const d360_group *g, const float *depth, const float *normal,
+                    float *cost_out, void *stream);
+
+/* replaces kernels.red_black_pass (K:352-473; callers E:403-420, E:578-595).
+ * Unlike the reference the caller need NOT pre-copy in->out: off-parity pixels are
+ * copied by the kernel.  n_evals (device, optional, uint64) is incremented by the number
+ * of cost evaluations executed (duplicate candidates skipped, K:418-432). */
+int d360_red_black_pass(const d360_group *g, int parity, const float *depth_in,
+                        const float *normal_in, const float *cost_in, float *depth_out,
+                        float *normal_out, float *cost_out, unsigned long long *n_evals,
+                        void *stream);
+
+/* replaces kernels.refine_pass (K:476-610; caller E:602-621).  cand_* are host arrays of
+ * n_cand floats (E:495-526).  In place. */
+int d360_refine_pass(const d360_group *g, float *depth, float *normal, float *cost,
+                     const float *cand_dd, const float *cand_sa, const float *cand_ca,
+                     const float *cand_caz, const float *cand_saz, int n_cand,
+                     double depth_min, double depth_max, void *stream);
+
+/* replaces the loop of engine.run_patchmatch (E:563-631): eval_costs, then `iterations`
+ * x (red, black, refine) with state resident on the device.  tables: host
+ * (iterations,5,n_cand) f32 in the order (dd, sin ang, cos ang, cos az, sin az).
+ * depth/normal in/out, cost out; scratch_* are caller-owned ping-pong buffers of the same
+ * shapes.  valid_out (optional, u8) = cost < trunc (E:629). */
+int d360_run_patchmatch(const d360_group *g, float *depth, float *normal, float *cost,
+                        float *scratch_depth, float *scratch_normal, float *scratch_cost,
+                        const float *tables, int iterations, int n_cand, double depth_min,
+                        double depth_max, uint8_t *valid_out, unsigned long long *n_evals,
+                        void *stream);
+
+/* replaces kernels.median_support_mask (K:613-647; caller E:634-648) */
+int d360_median_support_mask(const float *depth, const uint8_t *valid, int half,
+                             double rel_threshold, uint8_t *out_valid, int height, int width,
+                             void *stream);
+
+/* replaces keyframes.to_gray (KF:64-72).  channels = 1 or 3, image device u8. */
+int d360_to_gray(const uint8_t *image, int channels, float *gray, int height, int width,
+                 void *stream);
+
+/* replaces geometry.camera_rays (G:117-122).  Tables are device f64 arrays computed by the
+ * host exactly as G:81-86; rays32 (H,W,3) f32 and/or rays64 (H,W,3) f64 may be NULL. */
+int d360_camera_rays(const double *sin_lam, const double *cos_lam, const double *sin_phi,
+                     const double *cos_phi, float *rays32, double *rays64, int height,
+                     int width, void *stream);
+
+/* replaces engine.random_init (E:244-283).
+ * Injected mode (inv_draws/normal_draws non-NULL, device f64 (H,W) / (H,W,3)): applies the
+ * reference transform to host-generated NumPy PCG64 draws -> identical hypotheses.
+ * Native mode (both NULL): counter-based Philox4x32-10 keyed by `seed`, counter = pixel
+ * index; same distributions (uniform inverse depth, uniform facing hemisphere).
+ * Fills only pixels with valid==0, sets their cost to +inf, then marks all valid. */
+int d360_random_init(float *depth, float *normal, float *cost, uint8_t *valid,
+                     const double *inv_draws, const double *normal_draws, uint64_t seed,
+                     double depth_min, double depth_max, const double *rays64, int height,
+                     int width, void *stream);
+
+/* replaces engine.warp_plane_map (E:286-355).  r_rel/t_rel host f64 from
+ * relative_transform(pose_prev, pose_cur).  Outputs are fully overwritten (unfilled pixels
+ * get depth 0, normal 0, cost +inf, valid 0).  winner: device scratch (H,W) uint64. */
+int d360_warp_plane_map(const float *src_depth, const float *src_normal,
+                        const float *src_cost, const uint8_t *src_valid, const double *rays64,
+                        const double *r_rel, const double *t_rel, double depth_min,
+                        double depth_max, float *out_depth, float *out_normal, float *out_cost,
+                        uint8_t *out_valid, unsigned long long *winner, int height, int width,
+                        void *stream);
+
+/* rows with |latitude| > limit_deg are invalidated in place */
+int d360_pole_mask(uint8_t *valid, double limit_deg, int height, int width, void *stream);
+
+/* replaces pipeline.consistency_filter.  Window frames: device depth/valid
+ * pointers per frame (host arrays of n_frames pointers), poses host f64 (n_frames,9)/(n_frames,3)
+ * camera->world. */
+int d360_consistency_filter(const float *depth, const uint8_t *valid, const double *rot,
+                            const double *trans, const float *const *win_depth,
+                            const uint8_t *const *win_valid, const double *win_rot,
+                            const double *win_trans, int n_frames, const double *rays64,
+                            int min_support, double rel_tol, uint8_t *out_valid, int height,
+                            int width, void *stream);
+
+/* replaces FusionBuffer._fuse_oldest.  Emits surviving points in row-major
+ * order of the oldest frame (np.nonzero order): points (N,3) f64, colors (N,3) u8.
+ * keep (H,W) u8 and block_counts (device uint32, >= d360_fuse_blocks(H,W)+1 entries) are
+ * scratch; *n_points_host receives N (this call synchronises the stream once). */
+int d360_fuse_blocks(int height, int width);
+int d360_fuse_oldest(const float *depth, const uint8_t *valid, const double *rot,
+                     const double *trans, const uint8_t *image_rgb,
+                     const float *const *newer_depth, const uint8_t *const *newer_valid,
+                     const double *newer_rot, const double *newer_trans, int n_newer,
+                     const double *rays64, double reproj_px, double rel_tol, uint8_t *keep,
+                     uint32_t *block_counts, double *points, uint8_t *colors,
+                     int64_t *n_points_host, int height, int width, void *stream);
+
+/* replaces synth.render_scene for box/corridor scenes (SY:66-84, SY:101-169): analytic
+ * ray cast + 4-octave splitmix value noise, f64; image (H,W,3) u8, depth (H,W) f32. */
+int d360_render_box_scene(const double *size_xyz, int texture_seed, double noise_scale,
+                          int octaves, const double *rot, const double *trans,
+                          const double *rays64, uint8_t *image, float *depth, int height,
+                          int width, void *stream);
+
+/* FP32-FMA peak microbenchmark used as the roofline denominator for the cost kernels
+ * (MEASURED_PEAKS.json carries no FP32 figure).  Returns achieved TFLOP/s (FMA = 2),
+ * fp64 != 0 measures the DFMA pipe instead.  Synchronous. */
+double d360_measure_fma_peak(int fp64, int iters);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* D360_H */

@@ -1,0 +1,100 @@
+"""ctypes binding of libd360.so — the C ABI declared in include/d360.h.
+
+The library is the product: if it is missing or cannot be loaded this module raises
+BackendError.  Nothing here (or anywhere in the package) falls back to a CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+from .errors import BackendError
+
+PREC_EXACT = 0
+PREC_MIXED = 1
+
+MAX_VIEWS = 8
+MAX_SAMPLES = 128
+MAX_REFINE = 16
+MAX_FRAMES = 8
+
+_LIB_PATH = Path(__file__).resolve().parent / "libd360.so"
+_lib = None
+
+c_void = C.c_void_p
+
+
+class Group(C.Structure):
+    """struct d360_group"""
+
+    _fields_ = [
+        ("width", C.c_int32), ("height", C.c_int32), ("n_views", C.c_int32), ("n_samples", C.c_int32),
+        ("top_k", C.c_int32), ("precision", C.c_int32),
+        ("rays", c_void), ("ref_gray", c_void), ("nb", c_void),
+        ("rel_r", c_void), ("rel_t", c_void), ("offsets", c_void),
+        ("trunc", C.c_double),
+    ]
+
+
+_SIGNATURES = {
+    "d360_last_error": (C.c_char_p, []),
+    "d360_version": (C.c_int, []),
+    "d360_eval_costs": (C.c_int, [C.POINTER(Group), c_void, c_void, c_void, c_void]),
+    "d360_red_black_pass": (C.c_int, [C.POINTER(Group), C.c_int] + [c_void] * 8),
+    "d360_refine_pass": (C.c_int, [C.POINTER(Group)] + [c_void] * 8 + [C.c_int, C.c_double, C.c_double, c_void]),
+    "d360_run_patchmatch": (C.c_int, [C.POINTER(Group)] + [c_void] * 7 + [C.c_int, C.c_int, C.c_double,
+                                                                         C.c_double, c_void, c_void, c_void]),
+    "d360_median_support_mask": (C.c_int, [c_void, c_void, C.c_int, C.c_double, c_void, C.c_int, C.c_int, c_void]),
+    "d360_to_gray": (C.c_int, [c_void, C.c_int, c_void, C.c_int, C.c_int, c_void]),
+    "d360_camera_rays": (C.c_int, [c_void] * 6 + [C.c_int, C.c_int, c_void]),
+    "d360_random_init": (C.c_int, [c_void] * 6 + [C.c_uint64, C.c_double, C.c_double, c_void, C.c_int, C.c_int,
+                                                  c_void]),
+    "d360_warp_plane_map": (C.c_int, [c_void] * 7 + [C.c_double, C.c_double] + [c_void] * 5 + [C.c_int, C.c_int,
+                                                                                              c_void]),
+    "d360_pole_mask": (C.c_int, [c_void, C.c_double, C.c_int, C.c_int, c_void]),
+    "d360_consistency_filter": (C.c_int, [c_void] * 8 + [C.c_int, c_void, C.c_int, C.c_double, c_void, C.c_int,
+                                                         C.c_int, c_void]),
+    "d360_fuse_blocks": (C.c_int, [C.c_int, C.c_int]),
+    "d360_fuse_oldest": (C.c_int, [c_void] * 9 + [C.c_int, c_void, C.c_double, C.c_double] + [c_void] * 5 +
+                         [C.c_int, C.c_int, c_void]),
+    "d360_render_box_scene": (C.c_int, [c_void, C.c_int, C.c_double, C.c_int, c_void, c_void, c_void, c_void,
+                                        c_void, C.c_int, C.c_int, c_void]),
+    "d360_measure_fma_peak": (C.c_double, [C.c_int, C.c_int]),
+}
+
+EXPORTED_SYMBOLS = tuple(_SIGNATURES)
+
+
+def lib_path() -> Path:
+    return _LIB_PATH
+
+
+def load():
+    """Load libd360.so once; raise BackendError if it is absent (no fallback exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not _LIB_PATH.exists():
+        raise BackendError(
+            f"{_LIB_PATH} is missing: build it with `python -m paper_2211_16266_b200._build` "
+            "(nvcc, sm_100a).  This package has no CPU fallback."
+        )
+    try:
+        lib = C.CDLL(str(_LIB_PATH))
+    except OSError as exc:
+        raise BackendError(f"cannot load {_LIB_PATH}: {exc}") from exc
+    for name, (restype, argtypes) in _SIGNATURES.items():
+        try:
+            fn = getattr(lib, name)
+        except AttributeError as exc:
+            raise BackendError(f"{_LIB_PATH} does not export {name}") from exc
+        fn.restype = restype
+        fn.argtypes = argtypes
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = load().d360_last_error()
+        raise BackendError(f"{what} failed (status {rc}): {msg.decode() if msg else 'unknown error'}")

@@ -1,0 +1,130 @@
+// Error reporting, parameter validation and the FMA-peak microbenchmark.
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include "d360_device.cuh"
+
+namespace d360 {
+
+static thread_local char g_error[512] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_error, sizeof(g_error), fmt, ap);
+    va_end(ap);
+}
+
+int check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error("%s: CUDA launch failed: %s", what, cudaGetErrorString(e));
+        return 2;
+    }
+    return 0;
+}
+
+int make_group_dev(const d360_group* g, GroupDev* out) {
+    if (g == nullptr) { set_error("group is NULL"); return 1; }
+    if (g->width < 2 || g->height < 2) {
+        set_error("camera size must be at least 2x2, got %dx%d", g->width, g->height);
+        return 1;
+    }
+    if (g->n_views < 1 || g->n_views > D360_MAX_VIEWS) {
+        set_error("n_views %d outside [1, %d]", g->n_views, D360_MAX_VIEWS);
+        return 1;
+    }
+    if (g->n_samples < 1 || g->n_samples > D360_MAX_SAMPLES) {
+        set_error("n_samples %d outside [1, %d]", g->n_samples, D360_MAX_SAMPLES);
+        return 1;
+    }
+    if (g->top_k < 1 || g->top_k > g->n_views) {
+        set_error("top_k %d outside [1, n_views=%d]", g->top_k, g->n_views);
+        return 1;
+    }
+    if (g->precision != D360_PREC_EXACT && g->precision != D360_PREC_MIXED) {
+        set_error("unsupported precision policy %d", g->precision);
+        return 1;
+    }
+    if (!(g->trunc > 0.0)) { set_error("cost_truncation must be > 0, got %g", g->trunc); return 1; }
+    if (!g->rays || !g->ref_gray || !g->nb || !g->rel_r || !g->rel_t || !g->offsets) {
+        set_error("group has a NULL array pointer");
+        return 1;
+    }
+    GroupDev& d = *out;
+    d.W = g->width; d.H = g->height; d.V = g->n_views; d.S = g->n_samples; d.top_k = g->top_k;
+    d.rays = g->rays; d.ref_gray = g->ref_gray; d.nb = g->nb; d.trunc = g->trunc;
+    int reach = 0;
+    for (int k = 0; k < g->n_samples; ++k) {
+        const int dx = g->offsets[2 * k], dy = g->offsets[2 * k + 1];
+        if (abs(dx) > D360_MAX_REACH || abs(dy) > D360_MAX_REACH) {
+            set_error("sample offset (%d,%d) exceeds the supported reach %d", dx, dy, D360_MAX_REACH);
+            return 1;
+        }
+        if (abs(dx) >= g->width) {
+            set_error("sample offset dx=%d does not fit width %d (single wrap, K:169-172)", dx, g->width);
+            return 1;
+        }
+        reach = abs(dx) > reach ? abs(dx) : reach;
+        reach = abs(dy) > reach ? abs(dy) : reach;
+        d.dx[k] = (signed char)dx;
+        d.dy[k] = (signed char)dy;
+    }
+    d.reach = reach;
+    for (int v = 0; v < g->n_views; ++v) {
+        for (int i = 0; i < 9; ++i) d.rel_r[v][i] = g->rel_r[9 * v + i];
+        for (int i = 0; i < 3; ++i) d.rel_t[v][i] = g->rel_t[3 * v + i];
+    }
+    return 0;
+}
+
+// ---------------------------------------------------------------------------------------
+// FMA-pipe peak: 16 independent accumulator chains per thread, 8 CTAs of 256 per SM.
+// ---------------------------------------------------------------------------------------
+template <typename T>
+__global__ void k_fma_peak(T* out, int iters, T a, T b) {
+    T acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = (T)(threadIdx.x + i);
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] = acc[i] * a + b;
+    }
+    T s = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s += acc[i];
+    if (s == (T)123456789) out[0] = s;  // never true; keeps the chains alive
+}
+
+}  // namespace d360
+
+extern "C" const char* d360_last_error(void) { return d360::g_error; }
+extern "C" int d360_version(void) { return 100; }
+
+extern "C" double d360_measure_fma_peak(int fp64, int iters) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    void* out = nullptr;
+    if (cudaMalloc(&out, 64) != cudaSuccess) return -1.0;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int blocks = sms * 8, threads = 256;
+    float best_ms = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+        cudaEventRecord(e0);
+        if (fp64) d360::k_fma_peak<double><<<blocks, threads>>>((double*)out, iters, 1.0000001, 1e-9);
+        else d360::k_fma_peak<float><<<blocks, threads>>>((float*)out, iters, 1.0000001f, 1e-9f);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (rep > 0 && ms < best_ms) best_ms = ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    const double flops = 2.0 * 16.0 * (double)iters * (double)blocks * threads;
+    return flops / (best_ms * 1e-3) / 1e12;
+}

@@ -1,0 +1,536 @@
+"""Plane-hypothesis stereo for one equirectangular reference keyframe — host side.
+
+Mirrors the public surface of the reference's ``densify360.engine`` (E = engine.py there):
+``PatchSpec``, ``PlaneMap``, ``DepthPanorama``, ``prepare_group``, ``random_init``,
+``warp_plane_map``, ``red_black_iteration``, ``run_patchmatch``, ``median_outlier_filter``.
+The numpy-facing functions keep the reference's argument meaning and error behaviour; every
+per-pixel computation is a CUDA kernel behind the C ABI of ``include/d360.h``.  State can
+also stay on the device between calls (``DevicePlaneMap`` and the ``*_device`` functions),
+which is what ``DepthStage`` and the benchmark use.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import BackendError, ConfigError
+from .geometry import EquirectCamera, RigidPose, relative_transform, trig_tables
+from .keyframes import StereoGroup
+
+DEFAULT_REFINE_THETA_DEG = 60.0  # E:29
+DEFAULT_REFINE_DEPTH_FRACTION = 0.25  # E:30
+REFINE_CANDIDATES = 6  # E:31
+
+PRECISIONS = {"exact": _lib.PREC_EXACT, "mixed": _lib.PREC_MIXED}
+DEFAULT_PRECISION = "mixed"
+
+
+def default_top_k(n_views: int) -> int:
+    """V <= 2: every view (the reference's plain mean, K:297); V > 2: the better half."""
+    return n_views if n_views <= 2 else max(2, n_views // 2)
+
+
+# ---------------------------------------------------------------------------------------
+# device plumbing
+# ---------------------------------------------------------------------------------------
+
+def _device(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise BackendError("no CUDA device is visible; this package has no CPU fallback")
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device(device)
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else t.data_ptr()
+
+
+def _up(a: np.ndarray, dtype, device) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=dtype)).to(device, non_blocking=False)
+
+
+class DeviceCamera:
+    """Per-(camera, device) constants: trig tables and pixel rays in f32 and f64."""
+
+    _cache: dict = {}
+
+    def __init__(self, camera: EquirectCamera, device: torch.device):
+        lib = _lib.load()
+        self.camera = camera
+        self.device = device
+        h, w = camera.shape
+        with torch.cuda.device(device):
+            tabs = [_up(t, np.float64, device) for t in trig_tables(camera)]
+            self.rays32 = torch.empty((h, w, 3), dtype=torch.float32, device=device)
+            self.rays64 = torch.empty((h, w, 3), dtype=torch.float64, device=device)
+            _lib.check(lib.d360_camera_rays(_ptr(tabs[0]), _ptr(tabs[1]), _ptr(tabs[2]), _ptr(tabs[3]),
+                                            _ptr(self.rays32), _ptr(self.rays64), h, w, _stream()),
+                       "camera_rays")
+            torch.cuda.current_stream().synchronize()
+
+    @classmethod
+    def get(cls, camera: EquirectCamera, device=None) -> "DeviceCamera":
+        dev = _device(device)
+        key = (camera.width, camera.height, dev.index)
+        if key not in cls._cache:
+            cls._cache[key] = cls(camera, dev)
+        return cls._cache[key]
+
+
+# ---------------------------------------------------------------------------------------
+# value types (reference E:34-134)
+# ---------------------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class PatchSpec:
+    """Patch sampling grid and cost truncation (E:34-65)."""
+
+    half_window: int = 5
+    sample_stride: int = 2
+    cost_truncation: float = 1.2
+
+    def __post_init__(self) -> None:
+        if self.half_window < 1:
+            raise ConfigError(f"patchmatch.half_window must be >= 1, got {self.half_window}")
+        if self.sample_stride < 1:
+            raise ConfigError(f"patchmatch.sample_stride must be >= 1, got {self.sample_stride}")
+        if not self.cost_truncation > 0:
+            raise ConfigError(f"patchmatch.cost_truncation must be > 0, got {self.cost_truncation}")
+
+    def sample_offsets(self) -> np.ndarray:
+        """(S, 2) int32 (dx, dy), dy outer / dx inner (E:60-65)."""
+        reach = (self.half_window // self.sample_stride) * self.sample_stride
+        steps = np.arange(-reach, reach + 1, self.sample_stride, dtype=np.int32)
+        grid_y, grid_x = np.meshgrid(steps, steps, indexing="ij")
+        return np.stack([grid_x.ravel(), grid_y.ravel()], axis=1).astype(np.int32)
+
+
+@dataclass
+class PlaneMap:
+    """Host (numpy) plane hypotheses + cost + validity (E:68-118)."""
+
+    camera: EquirectCamera
+    depth: np.ndarray
+    normal: np.ndarray
+    cost: np.ndarray
+    valid: np.ndarray
+    depth_range: tuple
+
+    @classmethod
+    def empty(cls, camera: EquirectCamera, depth_range) -> "PlaneMap":
+        h, w = camera.shape
+        return cls(camera, np.zeros((h, w), np.float32), np.zeros((h, w, 3), np.float32),
+                   np.full((h, w), np.inf, np.float32), np.zeros((h, w), bool), tuple(depth_range))
+
+    @property
+    def width(self) -> int:
+        return self.camera.width
+
+    @property
+    def height(self) -> int:
+        return self.camera.height
+
+    def copy(self) -> "PlaneMap":
+        return PlaneMap(self.camera, self.depth.copy(), self.normal.copy(), self.cost.copy(),
+                        self.valid.copy(), self.depth_range)
+
+    def hypothesis(self, x: int, y: int):
+        from .geometry import PlaneHypothesis
+
+        return PlaneHypothesis(depth=float(self.depth[y, x]), normal=self.normal[y, x].astype(np.float64))
+
+
+@dataclass
+class DepthPanorama:
+    """Dense depth + validity (E:121-134)."""
+
+    camera: EquirectCamera
+    depth: np.ndarray
+    valid: np.ndarray
+
+    def copy(self) -> "DepthPanorama":
+        return DepthPanorama(self.camera, self.depth.copy(), self.valid.copy())
+
+    @property
+    def valid_count(self) -> int:
+        return int(self.valid.sum())
+
+
+class DevicePlaneMap:
+    """PlaneMap whose arrays live in HBM: depth (H,W) f32, normal (H,W,3) f32, cost (H,W) f32,
+    valid (H,W) u8 — the same layouts as the numpy type, 21 B per pixel."""
+
+    def __init__(self, camera, depth, normal, cost, valid, depth_range):
+        self.camera = camera
+        self.depth, self.normal, self.cost, self.valid = depth, normal, cost, valid
+        self.depth_range = tuple(depth_range)
+
+    @classmethod
+    def empty(cls, camera: EquirectCamera, depth_range, device=None) -> "DevicePlaneMap":
+        dev = _device(device)
+        h, w = camera.shape
+        return cls(camera, torch.zeros((h, w), dtype=torch.float32, device=dev),
+                   torch.zeros((h, w, 3), dtype=torch.float32, device=dev),
+                   torch.full((h, w), float("inf"), dtype=torch.float32, device=dev),
+                   torch.zeros((h, w), dtype=torch.uint8, device=dev), depth_range)
+
+    @classmethod
+    def from_host(cls, pm: PlaneMap, device=None) -> "DevicePlaneMap":
+        dev = _device(device)
+        return cls(pm.camera, _up(pm.depth, np.float32, dev), _up(pm.normal, np.float32, dev),
+                   _up(pm.cost, np.float32, dev), _up(pm.valid.astype(np.uint8), np.uint8, dev), pm.depth_range)
+
+    def to_host(self) -> PlaneMap:
+        return PlaneMap(self.camera, self.depth.cpu().numpy(), self.normal.cpu().numpy(), self.cost.cpu().numpy(),
+                        self.valid.cpu().numpy().astype(bool), self.depth_range)
+
+    def clone(self) -> "DevicePlaneMap":
+        return DevicePlaneMap(self.camera, self.depth.clone(), self.normal.clone(), self.cost.clone(),
+                              self.valid.clone(), self.depth_range)
+
+    @property
+    def device(self):
+        return self.depth.device
+
+
+class DeviceDepthPanorama:
+    def __init__(self, camera, depth, valid):
+        self.camera, self.depth, self.valid = camera, depth, valid
+
+    def to_host(self) -> DepthPanorama:
+        return DepthPanorama(self.camera, self.depth.cpu().numpy(), self.valid.cpu().numpy().astype(bool))
+
+    @classmethod
+    def from_host(cls, p: DepthPanorama, device=None) -> "DeviceDepthPanorama":
+        dev = _device(device)
+        return cls(p.camera, _up(p.depth, np.float32, dev), _up(p.valid.astype(np.uint8), np.uint8, dev))
+
+
+# ---------------------------------------------------------------------------------------
+# PreparedGroup (E:137-160): images -> luma on the device, rays, relative poses, offsets
+# ---------------------------------------------------------------------------------------
+
+def to_gray_device(image, device=None) -> torch.Tensor:
+    """uint8 (H,W) / (H,W,3) numpy array or CUDA tensor -> float32 luma on the device
+    (keyframes.py:64-72, float32 arithmetic)."""
+    dev = _device(device)
+    lib = _lib.load()
+    img = image if isinstance(image, torch.Tensor) else _up(np.asarray(image), np.uint8, dev)
+    if img.dtype != torch.uint8:
+        raise ValueError(f"expected a uint8 image, got {img.dtype}")
+    if img.ndim == 2:
+        ch = 1
+    elif img.ndim == 3 and img.shape[2] == 3:
+        ch = 3
+    else:
+        raise ValueError(f"expected (H, W) or (H, W, 3) image, got {tuple(img.shape)}")
+    img = img.contiguous()
+    h, w = img.shape[:2]
+    out = torch.empty((h, w), dtype=torch.float32, device=dev)
+    _lib.check(lib.d360_to_gray(_ptr(img), ch, _ptr(out), h, w, _stream()), "to_gray")
+    return out
+
+
+def to_gray(image: np.ndarray) -> np.ndarray:
+    """Drop-in for keyframes.to_gray (computed on the GPU)."""
+    return to_gray_device(image).cpu().numpy()
+
+
+class PreparedGroup:
+    """Stereo group unpacked into the kernel layout, resident on one GPU."""
+
+    def __init__(self, group: StereoGroup, spec: PatchSpec, top_k: int | None = None,
+                 precision: str | None = None, device=None, device_images=None):
+        self.group = group
+        self.spec = spec
+        self.camera = group.camera
+        self.device = _device(device)
+        self.n_views = len(group.neighbors)
+        self.top_k = default_top_k(self.n_views) if top_k is None else int(top_k)
+        if not 1 <= self.top_k <= self.n_views:
+            raise ConfigError(f"patchmatch.top_k must be in [1, {self.n_views}], got {self.top_k}")
+        self.precision = DEFAULT_PRECISION if precision is None else precision
+        if self.precision not in PRECISIONS:
+            raise ConfigError(f"patchmatch.precision must be one of {sorted(PRECISIONS)}, got {self.precision!r}")
+        self.offsets = spec.sample_offsets()
+        if len(self.offsets) > _lib.MAX_SAMPLES:
+            raise ConfigError(f"patch has {len(self.offsets)} samples; at most {_lib.MAX_SAMPLES} are supported")
+        with torch.cuda.device(self.device):
+            self.cam_dev = DeviceCamera.get(self.camera, self.device)
+            imgs = device_images if device_images is not None else (
+                [group.reference.image] + [nb.image for nb in group.neighbors])
+            self.ref_gray = to_gray_device(imgs[0], self.device)
+            self.nb = torch.stack([to_gray_device(im, self.device) for im in imgs[1:]]).contiguous()
+        rel = [relative_transform(group.reference.pose, nb.pose) for nb in group.neighbors]
+        self.rel_r = np.ascontiguousarray(np.stack([r for r, _ in rel]), dtype=np.float32)
+        self.rel_t = np.ascontiguousarray(np.stack([t for _, t in rel]), dtype=np.float32)
+        self._struct = _lib.Group(
+            width=self.camera.width, height=self.camera.height, n_views=self.n_views,
+            n_samples=len(self.offsets), top_k=self.top_k, precision=PRECISIONS[self.precision],
+            rays=_ptr(self.cam_dev.rays32), ref_gray=_ptr(self.ref_gray), nb=_ptr(self.nb),
+            rel_r=self.rel_r.ctypes.data, rel_t=self.rel_t.ctypes.data, offsets=self.offsets.ctypes.data,
+            trunc=float(spec.cost_truncation))
+
+    @property
+    def struct(self):
+        return C.byref(self._struct)
+
+
+def prepare_group(group: StereoGroup, spec: PatchSpec, **kw) -> PreparedGroup:
+    return PreparedGroup(group, spec, **kw)
+
+
+def _as_prepared(group, spec: PatchSpec) -> PreparedGroup:
+    return group if isinstance(group, PreparedGroup) else PreparedGroup(group, spec)
+
+
+# ---------------------------------------------------------------------------------------
+# random_init (E:244-283)
+# ---------------------------------------------------------------------------------------
+
+def _check_depth_range(depth_range):
+    dmin, dmax = float(depth_range[0]), float(depth_range[1])
+    if not (dmin > 0.0 and dmax > dmin):
+        raise ConfigError(f"patchmatch.depth_range must satisfy 0 < min < max, got [{dmin}, {dmax}]")
+    return dmin, dmax
+
+
+def random_init_device(pm: DevicePlaneMap, depth_range, seed: int, rng: str = "pcg64") -> DevicePlaneMap:
+    """Fill every invalid pixel in place with a random plane; mark everything valid.
+
+    rng="pcg64": the reference's NumPy draws are generated on the host and injected, so the
+    hypotheses are the reference's.  rng="philox": counter-based Philox4x32-10 on the device
+    (same distributions, no host work)."""
+    dmin, dmax = _check_depth_range(depth_range)
+    lib = _lib.load()
+    cam = DeviceCamera.get(pm.camera, pm.device)
+    h, w = pm.camera.shape
+    with torch.cuda.device(pm.device):
+        if rng == "pcg64":
+            gen = np.random.default_rng(seed)
+            inv = _up(gen.uniform(1.0 / dmax, 1.0 / dmin, size=(h, w)), np.float64, pm.device)
+            g = _up(gen.standard_normal((h, w, 3)), np.float64, pm.device)
+        elif rng == "philox":
+            inv = g = None
+        else:
+            raise ConfigError(f"rng must be 'pcg64' or 'philox', got {rng!r}")
+        _lib.check(lib.d360_random_init(_ptr(pm.depth), _ptr(pm.normal), _ptr(pm.cost), _ptr(pm.valid), _ptr(inv),
+                                        _ptr(g), int(seed) & 0xFFFFFFFFFFFFFFFF, dmin, dmax, _ptr(cam.rays64),
+                                        h, w, _stream()), "random_init")
+    pm.depth_range = (dmin, dmax)
+    return pm
+
+
+def random_init(plane_map: PlaneMap, depth_range, seed: int, rng: str = "pcg64") -> PlaneMap:
+    _check_depth_range(depth_range)
+    dev = DevicePlaneMap.from_host(plane_map)
+    return random_init_device(dev, depth_range, seed, rng).to_host()
+
+
+# ---------------------------------------------------------------------------------------
+# warp_plane_map (E:286-355)
+# ---------------------------------------------------------------------------------------
+
+def warp_plane_map_device(previous: DevicePlaneMap, pose_prev: RigidPose, pose_cur: RigidPose,
+                          camera: EquirectCamera) -> DevicePlaneMap:
+    if previous.camera != camera:
+        raise ConfigError(f"plane map camera {previous.camera} does not match target camera {camera}")
+    lib = _lib.load()
+    dev = previous.device
+    cam = DeviceCamera.get(camera, dev)
+    h, w = camera.shape
+    out = DevicePlaneMap(camera, torch.empty_like(previous.depth), torch.empty_like(previous.normal),
+                         torch.empty_like(previous.cost), torch.empty_like(previous.valid), previous.depth_range)
+    r_rel, t_rel = relative_transform(pose_prev, pose_cur)
+    r_rel = np.ascontiguousarray(r_rel, np.float64)
+    t_rel = np.ascontiguousarray(t_rel, np.float64)
+    with torch.cuda.device(dev):
+        winner = torch.empty((h, w), dtype=torch.int64, device=dev)
+        _lib.check(lib.d360_warp_plane_map(_ptr(previous.depth), _ptr(previous.normal), _ptr(previous.cost),
+                                           _ptr(previous.valid), _ptr(cam.rays64), r_rel.ctypes.data,
+                                           t_rel.ctypes.data, float(previous.depth_range[0]),
+                                           float(previous.depth_range[1]), _ptr(out.depth), _ptr(out.normal),
+                                           _ptr(out.cost), _ptr(out.valid), _ptr(winner), h, w, _stream()),
+                   "warp_plane_map")
+    return out
+
+
+def warp_plane_map(previous: PlaneMap, pose_prev: RigidPose, pose_cur: RigidPose, camera: EquirectCamera) -> PlaneMap:
+    return warp_plane_map_device(DevicePlaneMap.from_host(previous), pose_prev, pose_cur, camera).to_host()
+
+
+# ---------------------------------------------------------------------------------------
+# cost evaluation / propagation / refinement
+# ---------------------------------------------------------------------------------------
+
+def _check_initialized(valid_all: bool) -> None:
+    if not valid_all:
+        raise ConfigError("run_patchmatch requires a fully initialized plane map; "
+                          "fill unfilled pixels with random_init first")
+
+
+def evaluate_costs_device(prep: PreparedGroup, pm: DevicePlaneMap) -> None:
+    """cost <- matching cost of every pixel's hypothesis (kernels.eval_costs, K:300-349)."""
+    lib = _lib.load()
+    with torch.cuda.device(prep.device):
+        _lib.check(lib.d360_eval_costs(prep.struct, _ptr(pm.depth), _ptr(pm.normal), _ptr(pm.cost), _stream()),
+                   "eval_costs")
+
+
+def red_black_pass_device(prep: PreparedGroup, parity: int, src: DevicePlaneMap, dst: DevicePlaneMap,
+                          n_evals: torch.Tensor | None = None) -> None:
+    lib = _lib.load()
+    with torch.cuda.device(prep.device):
+        _lib.check(lib.d360_red_black_pass(prep.struct, int(parity), _ptr(src.depth), _ptr(src.normal),
+                                           _ptr(src.cost), _ptr(dst.depth), _ptr(dst.normal), _ptr(dst.cost),
+                                           _ptr(n_evals), _stream()), "red_black_pass")
+
+
+def refine_pass_device(prep: PreparedGroup, pm: DevicePlaneMap, table, depth_range) -> None:
+    lib = _lib.load()
+    dd, sa, ca, caz, saz = (np.ascontiguousarray(t, np.float32) for t in table)
+    with torch.cuda.device(prep.device):
+        _lib.check(lib.d360_refine_pass(prep.struct, _ptr(pm.depth), _ptr(pm.normal), _ptr(pm.cost),
+                                        dd.ctypes.data, sa.ctypes.data, ca.ctypes.data, caz.ctypes.data,
+                                        saz.ctypes.data, len(dd), float(depth_range[0]), float(depth_range[1]),
+                                        _stream()), "refine_pass")
+
+
+def red_black_iteration(plane_map: PlaneMap, group, spec: PatchSpec, parity) -> PlaneMap:
+    """One checkerboard pass on a host plane map (E:382-421)."""
+    parity_idx = {"red": 0, "black": 1, 0: 0, 1: 1}.get(parity)
+    if parity_idx is None:
+        raise ConfigError(f"parity must be 'red' or 'black', got {parity!r}")
+    _check_initialized(bool(plane_map.valid.all()))
+    prep = _as_prepared(group, spec)
+    cur = DevicePlaneMap.from_host(plane_map, prep.device)
+    if not np.isfinite(plane_map.cost).all():
+        evaluate_costs_device(prep, cur)
+    out = cur.clone()
+    red_black_pass_device(prep, parity_idx, cur, out)
+    return out.to_host()
+
+
+def refinement_draw_tables(seed: int, iterations: int, delta_d: float, theta: float) -> np.ndarray:
+    """(iterations, 5, 6) f32: rows (dd, sin ang, cos ang, cos az, sin az), drawn with NumPy
+    PCG64 in the reference's order so both paths share one schedule (E:495-526)."""
+    rng = np.random.default_rng(seed)
+    out = np.empty((iterations, 5, REFINE_CANDIDATES), np.float32)
+    for it in range(iterations):
+        draws = np.empty((REFINE_CANDIDATES, 3), np.float64)
+        for i in range(REFINE_CANDIDATES):
+            shrink = 0.5**i
+            draws[i, 0] = rng.uniform(-1.0, 1.0) * delta_d * shrink
+            draws[i, 1] = rng.uniform(0.0, 1.0) * theta * shrink
+            draws[i, 2] = rng.uniform(0.0, 2.0 * math.pi)
+        out[it, 0] = draws[:, 0].astype(np.float32)
+        out[it, 1] = np.sin(draws[:, 1]).astype(np.float32)
+        out[it, 2] = np.cos(draws[:, 1]).astype(np.float32)
+        out[it, 3] = np.cos(draws[:, 2]).astype(np.float32)
+        out[it, 4] = np.sin(draws[:, 2]).astype(np.float32)
+    return out
+
+
+class PatchMatchWorkspace:
+    """Ping-pong buffers and the evaluation counter reused across keyframes of one size."""
+
+    def __init__(self, camera: EquirectCamera, device):
+        h, w = camera.shape
+        self.depth = torch.empty((h, w), dtype=torch.float32, device=device)
+        self.normal = torch.empty((h, w, 3), dtype=torch.float32, device=device)
+        self.cost = torch.empty((h, w), dtype=torch.float32, device=device)
+        self.n_evals = torch.zeros((1,), dtype=torch.int64, device=device)
+
+
+def run_patchmatch_device(prep: PreparedGroup, pm: DevicePlaneMap, iterations: int, seed: int,
+                          refine_theta_deg: float = DEFAULT_REFINE_THETA_DEG,
+                          refine_depth_fraction: float = DEFAULT_REFINE_DEPTH_FRACTION,
+                          workspace: PatchMatchWorkspace | None = None, count_evals: bool = False,
+                          check_valid: bool = True):
+    """Optimise ``pm`` in place on the device; returns (pm, DeviceDepthPanorama).
+
+    One C-ABI call (d360_run_patchmatch) enqueues eval + iterations x (red, black, refine)."""
+    if iterations < 1:
+        raise ConfigError(f"patchmatch.iterations must be >= 1, got {iterations}")
+    if prep.camera != pm.camera:
+        raise ConfigError(f"plane map camera {pm.camera} does not match group camera {prep.camera}")
+    if check_valid:
+        _check_initialized(bool(pm.valid.all().item()))
+    lib = _lib.load()
+    dmin, dmax = pm.depth_range
+    tables = refinement_draw_tables(seed, iterations, refine_depth_fraction * (dmax - dmin),
+                                    math.radians(refine_theta_deg))
+    ws = workspace if workspace is not None else PatchMatchWorkspace(prep.camera, prep.device)
+    with torch.cuda.device(prep.device):
+        valid = torch.empty(prep.camera.shape, dtype=torch.uint8, device=prep.device)
+        if count_evals:
+            ws.n_evals.zero_()
+        _lib.check(lib.d360_run_patchmatch(prep.struct, _ptr(pm.depth), _ptr(pm.normal), _ptr(pm.cost),
+                                           _ptr(ws.depth), _ptr(ws.normal), _ptr(ws.cost), tables.ctypes.data,
+                                           int(iterations), REFINE_CANDIDATES, float(dmin), float(dmax),
+                                           _ptr(valid), _ptr(ws.n_evals) if count_evals else 0, _stream()),
+                   "run_patchmatch")
+    pano = DeviceDepthPanorama(prep.camera, pm.depth.clone(), valid)
+    return pm, pano
+
+
+def run_patchmatch(group, init: PlaneMap, spec: PatchSpec, iterations: int, seed: int, workers: int | None = None,
+                   refine_theta_deg: float = DEFAULT_REFINE_THETA_DEG,
+                   refine_depth_fraction: float = DEFAULT_REFINE_DEPTH_FRACTION):
+    """Drop-in for engine.run_patchmatch (E:529-631): host arrays in, host arrays out.
+
+    ``workers`` is accepted for signature compatibility and ignored (results never depended
+    on it, T/test_engine.py:478-488)."""
+    if iterations < 1:
+        raise ConfigError(f"patchmatch.iterations must be >= 1, got {iterations}")
+    _check_initialized(bool(np.asarray(init.valid).all()))
+    prep = _as_prepared(group, spec)
+    if prep.camera != init.camera:
+        raise ConfigError(f"plane map camera {init.camera} does not match group camera {prep.camera}")
+    pm = DevicePlaneMap.from_host(init, prep.device)
+    pm, pano = run_patchmatch_device(prep, pm, iterations, seed, refine_theta_deg, refine_depth_fraction,
+                                     check_valid=False)
+    return pm.to_host(), pano.to_host()
+
+
+# ---------------------------------------------------------------------------------------
+# median outlier filter (E:634-648)
+# ---------------------------------------------------------------------------------------
+
+def median_outlier_filter_device(pano: DeviceDepthPanorama, window: int = 5,
+                                 rel_threshold: float = 0.2) -> DeviceDepthPanorama:
+    if window < 3 or window % 2 == 0:
+        raise ConfigError(f"median filter window must be odd and >= 3, got {window}")
+    lib = _lib.load()
+    h, w = pano.camera.shape
+    out_valid = torch.empty_like(pano.valid)
+    with torch.cuda.device(pano.depth.device):
+        _lib.check(lib.d360_median_support_mask(_ptr(pano.depth), _ptr(pano.valid), window // 2,
+                                                float(rel_threshold), _ptr(out_valid), h, w, _stream()),
+                   "median_support_mask")
+    return DeviceDepthPanorama(pano.camera, pano.depth, out_valid)
+
+
+def median_outlier_filter(depth: DepthPanorama, window: int = 5, rel_threshold: float = 0.2) -> DepthPanorama:
+    if window < 3 or window % 2 == 0:
+        raise ConfigError(f"median filter window must be odd and >= 3, got {window}")
+    out = median_outlier_filter_device(DeviceDepthPanorama.from_host(depth), window, rel_threshold)
+    return DepthPanorama(depth.camera, depth.depth.copy(), out.valid.cpu().numpy().astype(bool))
+
+
+def pole_mask_device(pano: DeviceDepthPanorama, limit_deg: float) -> None:
+    """Invalidate rows beyond ``limit_deg`` of latitude in place."""
+    lib = _lib.load()
+    h, w = pano.camera.shape
+    with torch.cuda.device(pano.depth.device):
+        _lib.check(lib.d360_pole_mask(_ptr(pano.valid), float(limit_deg), h, w, _stream()), "pole_mask")

@@ -1,0 +1,109 @@
+"""Synthetic box / corridor scenes rendered on the GPU (benchmark and test input generator).
+
+Re-implements the analytic scenes of the reference's ``densify360.synth`` (SY = synth.py
+there): closed axis-aligned box viewed from inside (SY:66-84) textured with 4-octave
+splitmix-hash value noise (SY:101-151).  The kernel follows the float64 numpy code operation
+by operation, so for identity rotations the image is bit-identical to ``render_scene``
+(SY:154-169); the reference's CPU render takes ~11 s per 1920x960 frame.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .engine import DepthPanorama, DeviceCamera, _device, _ptr, _stream
+from .errors import ConfigError
+from .geometry import EquirectCamera, GeometryError, RigidPose
+from .keyframes import Keyframe, StereoGroup
+
+SCENE_KINDS = ("box", "corridor")
+
+
+@dataclass(frozen=True)
+class SyntheticScene:
+    """Axis-aligned box room: full extents in metres, value-noise texture parameters."""
+
+    kind: str = "box"
+    size: tuple = (4.0, 3.0, 5.0)
+    texture_seed: int = 7
+    noise_scale: float = 0.6
+    octaves: int = 4
+
+    def __post_init__(self) -> None:
+        if self.kind not in SCENE_KINDS:
+            raise ConfigError(f"scene kind must be one of {SCENE_KINDS}, got {self.kind!r}")
+        if min(self.size) <= 0:
+            raise ConfigError(f"scene size must be positive, got {self.size}")
+        if self.octaves < 1:
+            raise ConfigError(f"texture octaves must be >= 1, got {self.octaves}")
+
+    def contains(self, point, margin: float = 0.05) -> bool:
+        half = np.asarray(self.size, dtype=np.float64) / 2.0
+        return bool(np.all(np.abs(np.asarray(point, dtype=np.float64)) < half - margin))
+
+
+def default_scene(kind: str) -> SyntheticScene:
+    """Presets of SY:203-224."""
+    if kind == "box":
+        return SyntheticScene("box", (4.0, 3.0, 5.0))
+    if kind == "corridor":
+        return SyntheticScene("corridor", (4.0, 3.0, 20.0))
+    raise ConfigError(f"scene kind must be one of {SCENE_KINDS}, got {kind!r}")
+
+
+def render_scene_device(scene: SyntheticScene, camera: EquirectCamera, pose: RigidPose, device=None):
+    """(image (H,W,3) u8, depth (H,W) f32) as CUDA tensors."""
+    if not scene.contains(pose.translation):
+        raise GeometryError(f"camera at {pose.translation} lies outside the scene")
+    dev = _device(device)
+    lib = _lib.load()
+    cam = DeviceCamera.get(camera, dev)
+    h, w = camera.shape
+    size = np.ascontiguousarray(scene.size, dtype=np.float64)
+    rot = np.ascontiguousarray(pose.rotation.reshape(9), dtype=np.float64)
+    tr = np.ascontiguousarray(pose.translation, dtype=np.float64)
+    with torch.cuda.device(dev):
+        image = torch.empty((h, w, 3), dtype=torch.uint8, device=dev)
+        depth = torch.empty((h, w), dtype=torch.float32, device=dev)
+        _lib.check(lib.d360_render_box_scene(size.ctypes.data, int(scene.texture_seed), float(scene.noise_scale),
+                                             int(scene.octaves), rot.ctypes.data, tr.ctypes.data, _ptr(cam.rays64),
+                                             _ptr(image), _ptr(depth), h, w, _stream()), "render_box_scene")
+    return image, depth
+
+
+def render_scene(scene: SyntheticScene, camera: EquirectCamera, pose: RigidPose):
+    """Drop-in for synth.render_scene: (uint8 image, DepthPanorama) on the host."""
+    image, depth = render_scene_device(scene, camera, pose)
+    return image.cpu().numpy(), DepthPanorama(camera, depth.cpu().numpy(), np.ones(camera.shape, bool))
+
+
+def neighbor_offsets(n_views: int, step: float = 0.15):
+    """Signed baselines of SURVEY.md §8d: ±step, ±2 step, ... (V even) along one axis."""
+    offs = []
+    for k in range(1, n_views // 2 + 1):
+        offs += [-k * step, k * step]
+    if n_views % 2:
+        offs.append((n_views // 2 + 1) * step)
+    return offs
+
+
+def make_group(scene: SyntheticScene, camera: EquirectCamera, center=(0.0, 0.0, 0.0), n_views: int = 2,
+               step: float = 0.15, axis: int = 2, ref_id: int = 0, device=None):
+    """Reference keyframe at ``center`` plus ``n_views`` neighbours displaced along ``axis``.
+
+    Returns (StereoGroup, ground-truth depth (H,W) f32 numpy).  V=2 reproduces the layout of
+    the reference's test fixture (tests/scenes.py:11-29): neighbours at -step and +step."""
+    frames = []
+    gt = None
+    for k, off in enumerate([0.0] + neighbor_offsets(n_views, step)):
+        t = np.array(center, dtype=np.float64)
+        t[axis] += off
+        pose = RigidPose(np.eye(3), t)
+        image, pano = render_scene(scene, camera, pose)
+        frames.append(Keyframe(id=ref_id + k, image=image, pose=pose))
+        if k == 0:
+            gt = pano.depth
+    return StereoGroup(reference=frames[0], neighbors=tuple(frames[1:]), camera=camera), gt
