@@ -63,6 +63,15 @@ typedef struct d360_group {
 const char *d360_last_error(void);
 int d360_version(void);
 
+/* Instrumentation (the reference has only perf_counter stage clocks).
+ * d360_launch_count: kernels launched by this library since it was loaded.
+ * d360_trace_enable(1) clears the trace and starts bracketing every launch with CUDA
+ * events on its stream; d360_trace_summary synchronises them and writes one line per
+ * kernel kind, "<kind> <launches> <total_ms>\n", returning the byte count (-1 on error). */
+unsigned long long d360_launch_count(void);
+int d360_trace_enable(int on);
+int d360_trace_summary(char *buf, int cap);
+
 /* replaces kernels.eval_costs (K:300-349; caller E:366-379) */
 int d360_eval_costs(const d360_group *g, const float *depth, const float *normal,
                     float *cost_out, void *stream);

@@ -39,6 +39,9 @@ class Group(C.Structure):
 _SIGNATURES = {
     "d360_last_error": (C.c_char_p, []),
     "d360_version": (C.c_int, []),
+    "d360_launch_count": (C.c_ulonglong, []),
+    "d360_trace_enable": (C.c_int, [C.c_int]),
+    "d360_trace_summary": (C.c_int, [C.c_char_p, C.c_int]),
     "d360_eval_costs": (C.c_int, [C.POINTER(Group), c_void, c_void, c_void, c_void]),
     "d360_red_black_pass": (C.c_int, [C.POINTER(Group), C.c_int] + [c_void] * 8),
     "d360_refine_pass": (C.c_int, [C.POINTER(Group)] + [c_void] * 8 + [C.c_int, C.c_double, C.c_double, c_void]),
@@ -92,6 +95,29 @@ def load():
         fn.argtypes = argtypes
     _lib = lib
     return lib
+
+
+def launch_count() -> int:
+    """Kernels launched by libd360 since it was loaded."""
+    return int(load().d360_launch_count())
+
+
+def trace_enable(on: bool) -> None:
+    """Start (and clear) or stop per-launch CUDA-event timing inside the library."""
+    load().d360_trace_enable(1 if on else 0)
+
+
+def trace_summary() -> dict:
+    """{kernel kind: (launches, total device ms)} since trace_enable(True)."""
+    buf = C.create_string_buffer(1 << 16)
+    n = load().d360_trace_summary(buf, len(buf))
+    if n < 0:
+        check(1, "trace_summary")
+    out = {}
+    for line in buf.raw[:n].decode().splitlines():
+        kind, cnt, ms = line.split()
+        out[kind] = (int(cnt), float(ms))
+    return out
 
 
 def check(rc: int, what: str) -> None:

@@ -550,7 +550,10 @@ extern "C" int d360_to_gray(const uint8_t* image, int channels, float* gray, int
         return 1;
     }
     const size_t n = (size_t)height * width;
-    k_to_gray<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(image, channels, gray, n);
+    {
+        TraceScope ts_("to_gray", (cudaStream_t)stream);
+        k_to_gray<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(image, channels, gray, n);
+    }
     return check_launch("to_gray");
 }
 
@@ -558,8 +561,11 @@ extern "C" int d360_camera_rays(const double* sin_lam, const double* cos_lam, co
                                 const double* cos_phi, float* rays32, double* rays64, int height,
                                 int width, void* stream) {
     dim3 grid((width + 127) / 128, height);
-    k_camera_rays<<<grid, 128, 0, (cudaStream_t)stream>>>(sin_lam, cos_lam, sin_phi, cos_phi, rays32, rays64,
-                                                         height, width);
+    {
+        TraceScope ts_("camera_rays", (cudaStream_t)stream);
+        k_camera_rays<<<grid, 128, 0, (cudaStream_t)stream>>>(sin_lam, cos_lam, sin_phi, cos_phi, rays32, rays64,
+                                                             height, width);
+    }
     return check_launch("camera_rays");
 }
 
@@ -577,10 +583,16 @@ extern "C" int d360_random_init(float* depth, float* normal, float* cost, uint8_
     }
     const size_t n = (size_t)height * width;
     cudaStream_t s = (cudaStream_t)stream;
-    k_random_init<<<blocks_for(n, 256), 256, 0, s>>>(depth, normal, cost, valid, inv_draws, normal_draws, seed,
-                                                    1.0 / depth_max, 1.0 / depth_min, rays64, n);
+    {
+        TraceScope ts_("random_init", s);
+        k_random_init<<<blocks_for(n, 256), 256, 0, s>>>(depth, normal, cost, valid, inv_draws, normal_draws, seed,
+                                                        1.0 / depth_max, 1.0 / depth_min, rays64, n);
+    }
     if (check_launch("random_init")) return 2;
-    k_fill_u8<<<blocks_for(n, 256), 256, 0, s>>>(valid, 1, n);
+    {
+        TraceScope ts_("fill_u8", s);
+        k_fill_u8<<<blocks_for(n, 256), 256, 0, s>>>(valid, 1, n);
+    }
     return check_launch("random_init/valid");
 }
 
@@ -601,12 +613,18 @@ extern "C" int d360_warp_plane_map(const float* src_depth, const float* src_norm
         set_error("warp_plane_map: memset failed");
         return 2;
     }
-    k_warp_scatter<<<blocks_for(n, 256), 256, 0, s>>>(src_depth, src_normal, src_cost, src_valid, rays64, rel,
-                                                     depth_min, depth_max, winner, height, width);
+    {
+        TraceScope ts_("warp_scatter", s);
+        k_warp_scatter<<<blocks_for(n, 256), 256, 0, s>>>(src_depth, src_normal, src_cost, src_valid, rays64, rel,
+                                                         depth_min, depth_max, winner, height, width);
+    }
     if (check_launch("warp_plane_map/scatter")) return 2;
-    k_warp_gather<<<blocks_for(n, 256), 256, 0, s>>>(src_depth, src_normal, src_cost, rays64, rel, depth_min,
-                                                    depth_max, winner, out_depth, out_normal, out_cost,
-                                                    out_valid, height, width);
+    {
+        TraceScope ts_("warp_gather", s);
+        k_warp_gather<<<blocks_for(n, 256), 256, 0, s>>>(src_depth, src_normal, src_cost, rays64, rel, depth_min,
+                                                        depth_max, winner, out_depth, out_normal, out_cost,
+                                                        out_valid, height, width);
+    }
     return check_launch("warp_plane_map/gather");
 }
 
@@ -619,14 +637,20 @@ extern "C" int d360_median_support_mask(const float* depth, const uint8_t* valid
     }
     const size_t smem = (size_t)(MED_TW + 2 * half) * (MED_TH + 2 * half) * sizeof(float);
     dim3 grid((width + MED_TW - 1) / MED_TW, (height + MED_TH - 1) / MED_TH);
-    k_median<<<grid, MED_TW * MED_TH, smem, (cudaStream_t)stream>>>(depth, valid, half, rel_threshold, out_valid,
-                                                                   height, width);
+    {
+        TraceScope ts_("median", (cudaStream_t)stream);
+        k_median<<<grid, MED_TW * MED_TH, smem, (cudaStream_t)stream>>>(depth, valid, half, rel_threshold, out_valid,
+                                                                       height, width);
+    }
     return check_launch("median_support_mask");
 }
 
 extern "C" int d360_pole_mask(uint8_t* valid, double limit_deg, int height, int width, void* stream) {
     dim3 grid((width + 127) / 128, height);
-    k_pole_mask<<<grid, 128, 0, (cudaStream_t)stream>>>(valid, limit_deg, height, width);
+    {
+        TraceScope ts_("pole_mask", (cudaStream_t)stream);
+        k_pole_mask<<<grid, 128, 0, (cudaStream_t)stream>>>(valid, limit_deg, height, width);
+    }
     return check_launch("pole_mask");
 }
 
@@ -641,9 +665,12 @@ extern "C" int d360_consistency_filter(const float* depth, const uint8_t* valid,
     Frames win;
     if (fill_frames(&win, win_depth, win_valid, win_rot, win_trans, n_frames)) return 1;
     const size_t n = (size_t)height * width;
-    k_consistency<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(depth, valid, pose, win, rays64,
-                                                                       min_support, rel_tol, out_valid, height,
-                                                                       width);
+    {
+        TraceScope ts_("consistency", (cudaStream_t)stream);
+        k_consistency<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(depth, valid, pose, win, rays64,
+                                                                           min_support, rel_tol, out_valid, height,
+                                                                           width);
+    }
     return check_launch("consistency_filter");
 }
 
@@ -664,13 +691,22 @@ extern "C" int d360_fuse_oldest(const float* depth, const uint8_t* valid, const 
     if (fill_frames(&newer, newer_depth, newer_valid, newer_rot, newer_trans, n_newer)) return 1;
     cudaStream_t s = (cudaStream_t)stream;
     const int nb = d360_fuse_blocks(height, width);
-    k_fuse_mark<<<nb, FUSE_BLOCK, 0, s>>>(depth, valid, pose, newer, rays64, reproj_px, rel_tol, keep,
-                                         block_counts, height, width);
+    {
+        TraceScope ts_("fuse_mark", s);
+        k_fuse_mark<<<nb, FUSE_BLOCK, 0, s>>>(depth, valid, pose, newer, rays64, reproj_px, rel_tol, keep,
+                                             block_counts, height, width);
+    }
     if (check_launch("fuse/mark")) return 2;
-    k_scan_blocks<<<1, 1024, 0, s>>>(block_counts, nb);
+    {
+        TraceScope ts_("scan_blocks", s);
+        k_scan_blocks<<<1, 1024, 0, s>>>(block_counts, nb);
+    }
     if (check_launch("fuse/scan")) return 2;
-    k_fuse_emit<<<nb, FUSE_BLOCK, 0, s>>>(depth, keep, pose, image_rgb, rays64, block_counts, points, colors,
-                                         height, width);
+    {
+        TraceScope ts_("fuse_emit", s);
+        k_fuse_emit<<<nb, FUSE_BLOCK, 0, s>>>(depth, keep, pose, image_rgb, rays64, block_counts, points, colors,
+                                             height, width);
+    }
     if (check_launch("fuse/emit")) return 2;
     uint32_t total = 0;
     cudaError_t e = cudaMemcpyAsync(&total, block_counts + nb, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
@@ -694,6 +730,9 @@ extern "C" int d360_render_box_scene(const double* size_xyz, int texture_seed, d
     Rigid pose;
     fill_rigid(&pose, rot, trans);
     const size_t n = (size_t)height * width;
-    k_render_box<<<blocks_for(n, 128), 128, 0, (cudaStream_t)stream>>>(sc, pose, rays64, image, depth, n);
+    {
+        TraceScope ts_("render_box", (cudaStream_t)stream);
+        k_render_box<<<blocks_for(n, 128), 128, 0, (cudaStream_t)stream>>>(sc, pose, rays64, image, depth, n);
+    }
     return check_launch("render_box_scene");
 }

@@ -2,6 +2,11 @@
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
+
+#include <atomic>
+#include <mutex>
+#include <vector>
 
 #include "d360_device.cuh"
 
@@ -14,6 +19,48 @@ void set_error(const char* fmt, ...) {
     va_start(ap, fmt);
     vsnprintf(g_error, sizeof(g_error), fmt, ap);
     va_end(ap);
+}
+
+// ---------------------------------------------------------------------------------------
+// Launch accounting and optional per-launch device timing (the reference's only
+// instrumentation is a perf_counter per stage; here every kernel launch is
+// counted, and with tracing on it is bracketed by CUDA events on its own stream).
+// ---------------------------------------------------------------------------------------
+static std::atomic<unsigned long long> g_launches{0};
+static std::atomic<int> g_trace_on{0};
+struct TraceRec {
+    const char* kind;
+    cudaEvent_t e0, e1;
+};
+static std::mutex g_trace_mu;
+static std::vector<TraceRec> g_trace;
+static std::vector<cudaEvent_t> g_event_pool;
+
+static cudaEvent_t take_event() {
+    if (!g_event_pool.empty()) {
+        cudaEvent_t e = g_event_pool.back();
+        g_event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+TraceScope::TraceScope(const char* kind, cudaStream_t s) : idx_(-1), s_(s) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (!g_trace_on.load(std::memory_order_relaxed)) return;
+    std::lock_guard<std::mutex> lk(g_trace_mu);
+    TraceRec r{kind, take_event(), take_event()};
+    cudaEventRecord(r.e0, s_);
+    g_trace.push_back(r);
+    idx_ = (int)g_trace.size() - 1;
+}
+
+TraceScope::~TraceScope() {
+    if (idx_ < 0) return;
+    std::lock_guard<std::mutex> lk(g_trace_mu);
+    if (idx_ < (int)g_trace.size()) cudaEventRecord(g_trace[idx_].e1, s_);
 }
 
 int check_launch(const char* what) {
@@ -100,6 +147,54 @@ __global__ void k_fma_peak(T* out, int iters, T a, T b) {
 }  // namespace d360
 
 extern "C" const char* d360_last_error(void) { return d360::g_error; }
+
+extern "C" unsigned long long d360_launch_count(void) { return d360::g_launches.load(); }
+
+extern "C" int d360_trace_enable(int on) {
+    using namespace d360;
+    std::lock_guard<std::mutex> lk(g_trace_mu);
+    for (auto& r : g_trace) {
+        g_event_pool.push_back(r.e0);
+        g_event_pool.push_back(r.e1);
+    }
+    g_trace.clear();
+    g_trace_on.store(on ? 1 : 0);
+    return 0;
+}
+
+extern "C" int d360_trace_summary(char* buf, int cap) {
+    using namespace d360;
+    std::lock_guard<std::mutex> lk(g_trace_mu);
+    struct Agg { const char* kind; int n; double ms; };
+    std::vector<Agg> aggs;
+    for (auto& r : g_trace) {
+        if (cudaEventSynchronize(r.e1) != cudaSuccess) {
+            set_error("trace: event synchronize failed: %s", cudaGetErrorString(cudaGetLastError()));
+            return -1;
+        }
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.e0, r.e1);
+        Agg* a = nullptr;
+        for (auto& x : aggs)
+            if (strcmp(x.kind, r.kind) == 0) a = &x;
+        if (!a) {
+            aggs.push_back(Agg{r.kind, 0, 0.0});
+            a = &aggs.back();
+        }
+        a->n += 1;
+        a->ms += ms;
+    }
+    int off = 0;
+    for (auto& a : aggs) {
+        int w = snprintf(buf + off, off < cap ? cap - off : 0, "%s %d %.6f\n", a.kind, a.n, a.ms);
+        if (w < 0 || off + w >= cap) {
+            set_error("trace: summary buffer of %d bytes is too small", cap);
+            return -1;
+        }
+        off += w;
+    }
+    return off;
+}
 extern "C" int d360_version(void) { return 100; }
 
 extern "C" double d360_measure_fma_peak(int fp64, int iters) {

@@ -32,6 +32,19 @@ struct GroupDev {
     double trunc;
 };
 
+// Counts one kernel launch; when tracing is enabled (d360_trace_enable) also brackets it
+// with CUDA events on `s`.  Construct right before the <<<>>> launch, in its own scope.
+class TraceScope {
+public:
+    TraceScope(const char* kind, cudaStream_t s);
+    ~TraceScope();
+    TraceScope(const TraceScope&) = delete;
+    TraceScope& operator=(const TraceScope&) = delete;
+private:
+    int idx_;
+    cudaStream_t s_;
+};
+
 void set_error(const char* fmt, ...);
 int check_launch(const char* what);
 int make_group_dev(const d360_group* g, GroupDev* out);

@@ -452,7 +452,10 @@ static int launch_eval(const GroupDev& gd, int prec, const float* depth, const f
     D360_DISPATCH(prec, gd.V, {
         auto k = k_eval_costs<MODE, VT>;
         rc = prepare_kernel(k, smem);
-        if (!rc) k<<<grid, TILE_W * TILE_H, smem, s>>>(gd, depth, normal, cost_out);
+        if (!rc) {
+            TraceScope ts_("eval_costs", s);
+            k<<<grid, TILE_W * TILE_H, smem, s>>>(gd, depth, normal, cost_out);
+        }
     })
     return rc ? rc : check_launch("eval_costs");
 }
@@ -466,7 +469,10 @@ static int launch_red_black(const GroupDev& gd, int prec, int parity, const floa
     D360_DISPATCH(prec, gd.V, {
         auto k = k_red_black<MODE, VT>;
         rc = prepare_kernel(k, smem);
-        if (!rc) k<<<grid, RB_THREADS, smem, s>>>(gd, parity, di, ni, ci, dout, nout, cout, n_evals);
+        if (!rc) {
+            TraceScope ts_("red_black", s);
+            k<<<grid, RB_THREADS, smem, s>>>(gd, parity, di, ni, ci, dout, nout, cout, n_evals);
+        }
     })
     return rc ? rc : check_launch("red_black_pass");
 }
@@ -479,7 +485,10 @@ static int launch_refine(const GroupDev& gd, int prec, const RefineTable& tab, f
     D360_DISPATCH(prec, gd.V, {
         auto k = k_refine<MODE, VT>;
         rc = prepare_kernel(k, smem);
-        if (!rc) k<<<grid, TILE_W * TILE_H, smem, s>>>(gd, tab, depth, normal, cost, n_evals);
+        if (!rc) {
+            TraceScope ts_("refine", s);
+            k<<<grid, TILE_W * TILE_H, smem, s>>>(gd, tab, depth, normal, cost, n_evals);
+        }
     })
     return rc ? rc : check_launch("refine_pass");
 }
@@ -578,7 +587,10 @@ extern "C" int d360_run_patchmatch(const d360_group* g, float* depth, float* nor
     }
     if (valid_out != nullptr) {
         const size_t n = (size_t)gd.W * gd.H;
-        k_valid_from_cost<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(cc, (float)gd.trunc, valid_out, n);
+        {
+            TraceScope ts_("valid_from_cost", s);
+            k_valid_from_cost<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(cc, (float)gd.trunc, valid_out, n);
+        }
         if (check_launch("valid_from_cost")) return 1;
     }
     return 0;

@@ -220,9 +220,9 @@ class DeviceDepthPanorama:
 # PreparedGroup (E:137-160): images -> luma on the device, rays, relative poses, offsets
 # ---------------------------------------------------------------------------------------
 
-def to_gray_device(image, device=None) -> torch.Tensor:
+def to_gray_device(image, device=None, out: torch.Tensor | None = None) -> torch.Tensor:
     """uint8 (H,W) / (H,W,3) numpy array or CUDA tensor -> float32 luma on the device
-    (keyframes.py:64-72, float32 arithmetic)."""
+    (keyframes.py:64-72, float32 arithmetic).  ``out``: optional contiguous (H,W) f32 target."""
     dev = _device(device)
     lib = _lib.load()
     img = image if isinstance(image, torch.Tensor) else _up(np.asarray(image), np.uint8, dev)
@@ -236,7 +236,10 @@ def to_gray_device(image, device=None) -> torch.Tensor:
         raise ValueError(f"expected (H, W) or (H, W, 3) image, got {tuple(img.shape)}")
     img = img.contiguous()
     h, w = img.shape[:2]
-    out = torch.empty((h, w), dtype=torch.float32, device=dev)
+    if out is None:
+        out = torch.empty((h, w), dtype=torch.float32, device=dev)
+    elif out.shape != (h, w) or out.dtype != torch.float32 or not out.is_contiguous():
+        raise ValueError("out must be a contiguous float32 (H, W) tensor")
     _lib.check(lib.d360_to_gray(_ptr(img), ch, _ptr(out), h, w, _stream()), "to_gray")
     return out
 
@@ -269,8 +272,12 @@ class PreparedGroup:
             self.cam_dev = DeviceCamera.get(self.camera, self.device)
             imgs = device_images if device_images is not None else (
                 [group.reference.image] + [nb.image for nb in group.neighbors])
-            self.ref_gray = to_gray_device(imgs[0], self.device)
-            self.nb = torch.stack([to_gray_device(im, self.device) for im in imgs[1:]]).contiguous()
+            ref_img = imgs[0] if isinstance(imgs[0], torch.Tensor) else _up(np.asarray(imgs[0]), np.uint8, self.device)
+            self.ref_image = ref_img  # u8 (H,W) / (H,W,3) on the device; fusion reads its colours
+            self.ref_gray = to_gray_device(ref_img, self.device)
+            self.nb = torch.empty((self.n_views, *self.camera.shape), dtype=torch.float32, device=self.device)
+            for v, im in enumerate(imgs[1:]):
+                to_gray_device(im, self.device, out=self.nb[v])
         rel = [relative_transform(group.reference.pose, nb.pose) for nb in group.neighbors]
         self.rel_r = np.ascontiguousarray(np.stack([r for r, _ in rel]), dtype=np.float32)
         self.rel_t = np.ascontiguousarray(np.stack([t for _, t in rel]), dtype=np.float32)
@@ -459,7 +466,9 @@ def run_patchmatch_device(prep: PreparedGroup, pm: DevicePlaneMap, iterations: i
                           check_valid: bool = True):
     """Optimise ``pm`` in place on the device; returns (pm, DeviceDepthPanorama).
 
-    One C-ABI call (d360_run_patchmatch) enqueues eval + iterations x (red, black, refine)."""
+    One C-ABI call (d360_run_patchmatch) enqueues eval + iterations x (red, black, refine).
+    With ``count_evals`` the executed propagation/refinement cost evaluations are ADDED to
+    ``workspace.n_evals`` (zero it yourself; reading it synchronises)."""
     if iterations < 1:
         raise ConfigError(f"patchmatch.iterations must be >= 1, got {iterations}")
     if prep.camera != pm.camera:
@@ -473,8 +482,6 @@ def run_patchmatch_device(prep: PreparedGroup, pm: DevicePlaneMap, iterations: i
     ws = workspace if workspace is not None else PatchMatchWorkspace(prep.camera, prep.device)
     with torch.cuda.device(prep.device):
         valid = torch.empty(prep.camera.shape, dtype=torch.uint8, device=prep.device)
-        if count_evals:
-            ws.n_evals.zero_()
         _lib.check(lib.d360_run_patchmatch(prep.struct, _ptr(pm.depth), _ptr(pm.normal), _ptr(pm.cost),
                                            _ptr(ws.depth), _ptr(ws.normal), _ptr(ws.cost), tables.ctypes.data,
                                            int(iterations), REFINE_CANDIDATES, float(dmin), float(dmax),

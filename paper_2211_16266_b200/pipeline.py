@@ -150,7 +150,7 @@ class DepthStage:
     def __init__(self, camera: EquirectCamera, spec: PatchSpec, depth_range, iterations: int, seed: int,
                  warp: bool = True, workers: int | None = None, median_window: int = 5,
                  median_rel_threshold: float = 0.2, top_k: int | None = None, precision: str | None = None,
-                 init_rng: str = "pcg64", device=None):
+                 init_rng: str = "pcg64", device=None, count_evals: bool = False):
         self.camera, self.spec = camera, spec
         self.depth_range = tuple(depth_range)
         self.iterations, self.seed, self.warp, self.workers = iterations, seed, warp, workers
@@ -158,7 +158,12 @@ class DepthStage:
         self.top_k, self.precision, self.init_rng = top_k, precision, init_rng
         self.device = _device(device)
         self._prev: tuple | None = None
+        self.count_evals = count_evals
         self._ws = PatchMatchWorkspace(camera, self.device)
+
+    @property
+    def workspace(self) -> PatchMatchWorkspace:
+        return self._ws
 
     def process_device(self, group: StereoGroup | PreparedGroup) -> DeviceDepthResult:
         prep = group if isinstance(group, PreparedGroup) else PreparedGroup(
@@ -172,14 +177,14 @@ class DepthStage:
                 init = DevicePlaneMap.empty(self.camera, self.depth_range, self.device)
             init = random_init_device(init, self.depth_range, self.seed + ref.id, self.init_rng)
             plane_map, pano = run_patchmatch_device(prep, init, self.iterations, self.seed + ref.id,
-                                                    workspace=self._ws, check_valid=False)
+                                                    workspace=self._ws, count_evals=self.count_evals,
+                                                    check_valid=False)
             self._prev = (plane_map, ref.pose)
             pano = median_outlier_filter_device(pano, self.median_window, self.median_rel_threshold)
             pole_mask_device(pano, POLE_LAT_LIMIT_DEG)
-            img = np.asarray(ref.image)
-            if img.ndim == 2:
-                img = np.repeat(img[..., None], 3, axis=2)
-            image = _up(img, np.uint8, self.device)
+            image = prep.ref_image
+            if image.ndim == 2:
+                image = image[..., None].expand(-1, -1, 3).contiguous()
         return DeviceDepthResult(ref.id, pano, ref.pose, image)
 
     def process(self, group: StereoGroup) -> DepthResult:
