@@ -53,7 +53,13 @@ typedef struct d360_group {
     int32_t precision;          /* D360_PREC_* */
     const float *rays;          /* device (H,W,3) */
     const float *ref_gray;      /* device (H,W) */
-    const float *nb;            /* device (V,H,W) neighbour luma */
+    const float *nb;            /* device neighbour luma, V planes of (H + 2*nb_pad_y, W + 2*nb_pad_x):
+                                   the image with nb_pad_x wrapped columns on each side (the
+                                   panorama is periodic in x, K:141-150) and nb_pad_y replicated
+                                   rows above/below (v is clamped, K:143-147).  Pads 0 = dense
+                                   (V,H,W).  d360_to_gray_padded writes this layout; pads >= 1
+                                   enable the branch-free bilinear taps of the throughput kernels */
+    int32_t nb_pad_x, nb_pad_y;
     const float *rel_r;         /* host (V,3,3) x_nb = R x_ref + t (G:182-188), f32 (E:152) */
     const float *rel_t;         /* host (V,3) */
     const int32_t *offsets;     /* host (S,2) as (dx,dy) (E:60-65) */
@@ -111,6 +117,10 @@ int d360_median_support_mask(const float *depth, const uint8_t *valid, int half,
 /* replaces keyframes.to_gray (KF:64-72).  channels = 1 or 3, image device u8. */
 int d360_to_gray(const uint8_t *image, int channels, float *gray, int height, int width,
                  void *stream);
+/* same, written into the padded plane layout of d360_group.nb:
+ * gray is (height + 2*pad_y, width + 2*pad_x) */
+int d360_to_gray_padded(const uint8_t *image, int channels, float *gray, int height, int width,
+                        int pad_x, int pad_y, void *stream);
 
 /* replaces geometry.camera_rays (G:117-122).  Tables are device f64 arrays computed by the
  * host exactly as G:81-86; rays32 (H,W,3) f32 and/or rays64 (H,W,3) f64 may be NULL. */

@@ -14,19 +14,24 @@ namespace d360 {
 // ---------------------------------------------------------------------------------------
 // to_gray, keyframes.py:64-72 (float32 arithmetic, NumPy weak Python scalars)
 // ---------------------------------------------------------------------------------------
-__global__ void k_to_gray(const uint8_t* __restrict__ img, int channels, float* __restrict__ gray,
-                          size_t n) {
-    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    if (channels == 1) {
-        gray[i] = __fdiv_rn((float)img[i], 255.0f);
-    } else {
-        const float r = img[3 * i], g = img[3 * i + 1], b = img[3 * i + 2];
-        float acc = __fmul_rn(0.299f, r);
-        acc = __fadd_rn(acc, __fmul_rn(0.587f, g));
-        acc = __fadd_rn(acc, __fmul_rn(0.114f, b));
-        gray[i] = __fdiv_rn(acc, 255.0f);
-    }
+__device__ __forceinline__ float luma_of(const uint8_t* __restrict__ img, int channels, size_t i) {
+    if (channels == 1) return __fdiv_rn((float)img[i], 255.0f);
+    const float r = img[3 * i], g = img[3 * i + 1], b = img[3 * i + 2];
+    float acc = __fmul_rn(0.299f, r);
+    acc = __fadd_rn(acc, __fmul_rn(0.587f, g));
+    acc = __fadd_rn(acc, __fmul_rn(0.114f, b));
+    return __fdiv_rn(acc, 255.0f);
+}
+
+// Output raster (H + 2 pad_y, W + 2 pad_x): columns wrap, rows replicate (pads may be 0).
+__global__ void k_to_gray(const uint8_t* __restrict__ img, int channels, float* __restrict__ gray, int H, int W,
+                          int pad_x, int pad_y) {
+    const int pw = W + 2 * pad_x, ph = H + 2 * pad_y;
+    const int px = blockIdx.x * blockDim.x + threadIdx.x, py = blockIdx.y;
+    if (px >= pw || py >= ph) return;
+    const int x = pos_mod(px - pad_x, W);
+    const int y = min(max(py - pad_y, 0), H - 1);
+    gray[(size_t)py * pw + px] = luma_of(img, channels, (size_t)y * W + x);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -543,18 +548,27 @@ static int fill_frames(Frames* f, const float* const* depth, const uint8_t* cons
 
 using namespace d360;
 
-extern "C" int d360_to_gray(const uint8_t* image, int channels, float* gray, int height, int width,
-                            void* stream) {
+extern "C" int d360_to_gray_padded(const uint8_t* image, int channels, float* gray, int height, int width,
+                                   int pad_x, int pad_y, void* stream) {
     if (channels != 1 && channels != 3) {
         set_error("expected (H, W) or (H, W, 3) image, got %d channels", channels);
         return 1;
     }
-    const size_t n = (size_t)height * width;
+    if (pad_x < 0 || pad_y < 0 || pad_x > width) {
+        set_error("to_gray: pads must satisfy 0 <= pad_x <= width, 0 <= pad_y; got (%d, %d)", pad_x, pad_y);
+        return 1;
+    }
+    dim3 grid((width + 2 * pad_x + 255) / 256, height + 2 * pad_y);
     {
         TraceScope ts_("to_gray", (cudaStream_t)stream);
-        k_to_gray<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(image, channels, gray, n);
+        k_to_gray<<<grid, 256, 0, (cudaStream_t)stream>>>(image, channels, gray, height, width, pad_x, pad_y);
     }
     return check_launch("to_gray");
+}
+
+extern "C" int d360_to_gray(const uint8_t* image, int channels, float* gray, int height, int width,
+                            void* stream) {
+    return d360_to_gray_padded(image, channels, gray, height, width, 0, 0, stream);
 }
 
 extern "C" int d360_camera_rays(const double* sin_lam, const double* cos_lam, const double* sin_phi,

@@ -102,6 +102,11 @@ int make_group_dev(const d360_group* g, GroupDev* out) {
     GroupDev& d = *out;
     d.W = g->width; d.H = g->height; d.V = g->n_views; d.S = g->n_samples; d.top_k = g->top_k;
     d.rays = g->rays; d.ref_gray = g->ref_gray; d.nb = g->nb; d.trunc = g->trunc;
+    if (g->nb_pad_x < 0 || g->nb_pad_y < 0 || g->nb_pad_x > 64 || g->nb_pad_y > 64) {
+        set_error("neighbour plane pads (%d, %d) outside [0, 64]", g->nb_pad_x, g->nb_pad_y);
+        return 1;
+    }
+    d.nb_pad_x = g->nb_pad_x; d.nb_pad_y = g->nb_pad_y;
     int reach = 0;
     for (int k = 0; k < g->n_samples; ++k) {
         const int dx = g->offsets[2 * k], dy = g->offsets[2 * k + 1];

@@ -22,6 +22,7 @@ namespace d360 {
 // Kernel parameter block (passed by value; small arrays live in the constant bank).
 struct GroupDev {
     int W, H, V, S, top_k, reach;
+    int nb_pad_x, nb_pad_y;  // neighbour planes are (H + 2 pad_y, W + 2 pad_x), see d360.h
     const float* rays;
     const float* ref_gray;
     const float* nb;
@@ -44,6 +45,23 @@ private:
     int idx_;
     cudaStream_t s_;
 };
+
+// Shared refinement schedule of one pass (E:495-526), passed to the kernels by value.
+struct RefineTable {
+    float dd[D360_MAX_REFINE], sa[D360_MAX_REFINE], ca[D360_MAX_REFINE], caz[D360_MAX_REFINE],
+        saz[D360_MAX_REFINE];
+    int n;
+    double depth_min, depth_max;
+};
+
+// Throughput kernels (d360_fast.cu): policy MIXED on a regular sample grid.  Each returns -1
+// when it does not apply (irregular offsets, unsupported view count) and the caller falls
+// back to the generic kernels of d360_patchmatch.cu.
+int fast_eval(const struct GroupDev& gd, const float* depth, const float* normal, float* cost_out, cudaStream_t s);
+int fast_red_black(const struct GroupDev& gd, int parity, const float* di, const float* ni, const float* ci,
+                   float* dout, float* nout, float* cout, unsigned long long* n_evals, cudaStream_t s);
+int fast_refine(const struct GroupDev& gd, const RefineTable& tab, float* depth, float* normal, float* cost,
+                unsigned long long* n_evals, cudaStream_t s);
 
 void set_error(const char* fmt, ...);
 int check_launch(const char* what);

@@ -1,0 +1,581 @@
+// Throughput build of the PatchMatch cost kernels (precision policy D360_PREC_MIXED on a
+// regular sample grid) for sm_100a.
+//
+// Same algorithm and same decision rules as d360_patchmatch.cu (K:156-297, K:300-610), with
+// the per-sample-view instruction stream cut to what the B200's pipes need:
+//   * FP64 pipe (64 lanes/clk/SM, the binding resource): 47 operations per sample-view —
+//     t = lam * Rq + t_v, |t|^2, one third-order rsqrt / rcp refinement of the MUFU.64H
+//     seeds (error ~1e-18, no IEEE div/sqrt), the two degree-7 Horner chains of the
+//     reference's atan2 / acos polynomials, and the three NCC sums;
+//   * octant / hemisphere fix-ups of K:90-99 and K:129-131 are folded into one DFMA whose
+//     multiplier and addend come from 8- and 2-entry constant tables indexed by sign bits;
+//   * XU pipe (16 lanes/clk/SM): 3 MUFU.64H seeds + 3 F2F (u, v -> f32 as the reference's
+//     f32 scratch K:250-258, bilinear value -> f64); floor / frac of (u, v) use the
+//     1.5 * 2^23 magic-add on the FP32 pipe instead of F2I / I2F;
+//   * sample offsets come from loop counters (regular grid), all parameters from the
+//     constant bank, nothing is converted twice.
+// (u, v) are therefore the reference's f64 values to ~1e-12 px before the f32 rounding, which
+// is what holds the 1e-4 relative cost parity.
+#include <math.h>
+
+#include "d360_device.cuh"
+
+namespace d360 {
+namespace fast {
+
+constexpr int TW = 32;        // tile width (pixels)
+constexpr int TH_FULL = 8;    // tile height for eval / refine: 256 threads, one per pixel
+constexpr int TH_RB = 16;     // tile height for red-black: 256 threads, one per same-colour pixel
+constexpr int THREADS = 256;
+#ifndef D360_FAST_MINB
+#define D360_FAST_MINB 2
+#endif
+
+struct FastGroup {
+    int W, H, ns, stride, reach, top_k;
+    int pitch;            // neighbour plane row pitch (W + 2 pad_x), elements
+    unsigned max_idx;     // last index of a plane from which a 2x2 footprint may start
+    size_t plane;         // elements per neighbour plane
+    const float* rays;
+    const float* ref_gray;
+    const float* nb;      // padded planes, see d360.h
+    float rel_r[D360_MAX_VIEWS][9];
+    double rel_t[D360_MAX_VIEWS][3];
+    double mu[8], cu[8];  // longitude: u = p * mu[oct] + cu[oct]
+    double mv[2], cv[2];  // latitude:  v = p * mv[hem] + cv[hem]
+    double ca[8], cq[8];  // atan / acos polynomial coefficients, highest degree first (K:75-85, K:112-122)
+    double trunc, inv_s;
+    float pitch_f;        // pitch as float
+    float idx_bias;       // 2^23 + pad_y * pitch + pad_x: float -> index by mantissa extraction
+    float den_lim;        // largest f32 below -PARALLEL_EPS
+};
+
+struct Tile {
+    const float4* qg;  // (qx, qy, qz, reference luma) per window entry
+    const double* rq;  // [(v*3 + c) * ne + entry]
+    int ww, ne;
+};
+
+__host__ __device__ inline size_t tile_bytes(int tw, int th, int reach, int n_views) {
+    const size_t ne = (size_t)(tw + 2 * reach) * (th + 2 * reach);
+    return ne * sizeof(float4) + ne * sizeof(double) * 3 * n_views;
+}
+
+template <int VT>
+__device__ __forceinline__ Tile tile_setup(const FastGroup& g, unsigned char* smem, int x0, int y0, int th) {
+    const int R = g.reach;
+    const int ww = TW + 2 * R, hh = th + 2 * R, ne = ww * hh;
+    float4* qg = reinterpret_cast<float4*>(smem);
+    double* rq = reinterpret_cast<double*>(smem + (size_t)ne * sizeof(float4));
+    for (int e = threadIdx.x; e < ne; e += THREADS) {
+        const int j = e / ww, i = e - j * ww;
+        const int gx = pos_mod(x0 - R + i, g.W);
+        const int gy = min(max(y0 - R + j, 0), g.H - 1);
+        const size_t gi = (size_t)gy * g.W + gx;
+        const float bx = __ldg(g.rays + 3 * gi), by = __ldg(g.rays + 3 * gi + 1), bz = __ldg(g.rays + 3 * gi + 2);
+        qg[e] = make_float4(bx, by, bz, __ldg(g.ref_gray + gi));
+#pragma unroll
+        for (int v = 0; v < VT; ++v) {
+            const float* r = g.rel_r[v];
+            rq[(v * 3 + 0) * ne + e] = (double)dot3_f32(r[0], r[1], r[2], bx, by, bz);
+            rq[(v * 3 + 1) * ne + e] = (double)dot3_f32(r[3], r[4], r[5], bx, by, bz);
+            rq[(v * 3 + 2) * ne + e] = (double)dot3_f32(r[6], r[7], r[8], bx, by, bz);
+        }
+    }
+    Tile t;
+    t.qg = qg;
+    t.rq = rq;
+    t.ww = ww;
+    t.ne = ne;
+    return t;
+}
+
+// K:190-198 (f64 accumulation of the f32 luma and of its f32 square)
+__device__ __forceinline__ void pixel_stats(const FastGroup& g, const Tile& t, int ce, double& mr, double& sr) {
+    double acc = 0.0, acc2 = 0.0;
+    const int half = (g.ns - 1) / 2;
+    int e_row = ce - half * g.stride * (t.ww + 1);
+    for (int j = 0; j < g.ns; ++j) {
+        int e = e_row;
+        for (int i = 0; i < g.ns; ++i) {
+            const float v = t.qg[e].w;
+            acc = __dadd_rn(acc, (double)v);
+            acc2 = __dadd_rn(acc2, (double)__fmul_rn(v, v));
+            e += g.stride;
+        }
+        e_row += g.stride * t.ww;
+    }
+    const double m = acc * g.inv_s;  // S is a small integer: acc / S to <= 1 ulp, see note below
+    // the reference divides (acc / S); multiply-by-reciprocal differs by <= 1 ulp of f64,
+    // 12 orders below the parity tolerance.
+    double var = __dsub_rn(acc2 * g.inv_s, __dmul_rn(m, m));
+    var = var < 0.0 ? 0.0 : var;
+    mr = m;
+    sr = sqrt(var);
+}
+
+// 1/x, third-order refinement of the MUFU.RCP64H seed (2^-20 -> ~2^-60)
+__device__ __forceinline__ double rcp3(double x) {
+    const double y = rcp_seed(x);
+    const double e = fma(-x, y, 1.0);
+    return fma(y, fma(e, e, e), y);
+}
+// 1/sqrt(x), third-order refinement of the MUFU.RSQ64H seed
+__device__ __forceinline__ double rsqrt3(double x) {
+    const double y = rsqrt_seed(x);
+    const double e = fma(-(x * y), y, 1.0);
+    return fma(y * e, fma(e, 0.375, 0.5), y);
+}
+
+// (u, v) of K:244-258 for one neighbour-frame point t, rounded to f32 like the reference's
+// scratch.  No guards on the two measure-zero singularities (t on the neighbour's polar axis:
+// max(|tx|,|tz|) = 0 or 1 - |ty|/|t| <= 0); they yield NaN, which cand_cost maps to `trunc`.
+__device__ __forceinline__ void project(const FastGroup& g, double tx, double ty, double tz, float& pu, float& pv) {
+    // latitude: v = acos_poly(-ty / |t|) * H/pi - 0.5  (K:102-131)
+    const double r2 = fma(tz, tz, fma(ty, ty, fma(tx, tx, 1e-30)));
+    const double a = fabs(ty) * rsqrt3(r2);
+    double q = g.cq[0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) q = fma(a, q, g.cq[i]);
+    const double w = 1.0 - a;
+    const double sq = w * rsqrt3(w);
+    const int hem = (unsigned)__double2hiint(ty) >> 31 ^ 1;  // 1 when ty >= +0: sphi <= -0 (K:131)
+    pv = (float)fma(q * sq, g.mv[hem], g.cv[hem]);
+
+    // longitude: u = (atan2_poly(tx, tz) + pi) * W/2pi - 0.5  (K:59-99)
+    const unsigned hx = (unsigned)__double2hiint(tx), hz = (unsigned)__double2hiint(tz);
+    const bool swap = fabs(tx) > fabs(tz);
+    const double hi = swap ? tx : tz, lo = swap ? tz : tx;
+    const double r = lo * rcp3(hi);  // signed; only |r| is used (abs is a free operand modifier)
+    const double s = r * r;
+    double p = g.ca[0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) p = fma(s, p, g.ca[i]);
+    const int oct = (swap ? 1 : 0) + 2 * (hz >> 31) + 4 * (hx >> 31);
+    pu = (float)fma(fabs(r) * p, g.mu[oct], g.cu[oct]);
+}
+
+// K:134-153 on the f32 (u, v); weights and lerps in f32 (policy MIXED).  The plane is padded
+// (wrapped columns, replicated rows), so floor(u), floor(u)+1, floor(v), floor(v)+1 are all
+// in-plane and the reference's wrap / clamp rules are data, not code.  floor by the
+// 1.5 * 2^23 magic add; the element index is formed in f32 (exact below 2^23) and read out of
+// the mantissa, so no F2I / I2F conversions are issued.
+__device__ __forceinline__ float bilinear(const float* __restrict__ img, const FastGroup& g, float u, float v) {
+    const float MAGIC = 12582912.0f;
+    float fl_u = __fadd_rn(__fadd_rn(u, MAGIC), -MAGIC);
+    if (fl_u > u) fl_u -= 1.0f;
+    float fl_v = __fadd_rn(__fadd_rn(v, MAGIC), -MAGIC);
+    if (fl_v > v) fl_v -= 1.0f;
+    const float fu = u - fl_u, fv = v - fl_v;
+    const float off = __fadd_rn(fmaf(fl_v, g.pitch_f, fl_u), g.idx_bias);
+    const unsigned idx = min((unsigned)__float_as_int(off) & 0x7fffffu, g.max_idx);  // min: non-finite input only
+    const float* r0 = img + idx;
+    const float* r1 = img + (idx + g.pitch);
+    const float a = __ldg(r0), b = __ldg(r0 + 1), c = __ldg(r1), d = __ldg(r1 + 1);
+    const float top = fmaf(b - a, fu, a);
+    const float bot = fmaf(d - c, fu, c);
+    return fmaf(bot - top, fv, top);
+}
+
+template <int VT>
+__device__ __forceinline__ double aggregate(double (&cv)[VT], int top_k) {
+#pragma unroll
+    for (int i = 1; i < VT; ++i) {
+#pragma unroll
+        for (int j = i; j > 0; --j) {
+            const double lo = cv[j - 1] < cv[j] ? cv[j - 1] : cv[j];
+            const double hi = cv[j - 1] < cv[j] ? cv[j] : cv[j - 1];
+            cv[j - 1] = lo;
+            cv[j] = hi;
+        }
+    }
+    double total = 0.0;
+#pragma unroll
+    for (int i = 0; i < VT; ++i)
+        if (i < top_k) total = __dadd_rn(total, cv[i]);
+    return __dmul_rn(1.0 / top_k, total);
+}
+
+// Cost of one hypothesis at the pixel whose window entry is `ce` (K:201-297).
+template <int VT, typename HT>
+__device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, int ce, double mr, double sr, HT d,
+                                            HT nx, HT ny, HT nz) {
+    const double trunc = g.trunc;
+    const float4 a = t.qg[ce];
+    double num;
+    if constexpr (sizeof(HT) == 4) {
+        const float ndota = dot3_f32(nx, ny, nz, a.x, a.y, a.z);
+        if ((double)ndota >= -D360_FACING_EPS || sr < D360_SIGMA_EPS) return trunc;
+        num = (double)__fmul_rn(d, ndota);
+    } else {
+        const double ndota = dot3_f64(nx, ny, nz, (double)a.x, (double)a.y, (double)a.z);
+        if (ndota >= -D360_FACING_EPS || sr < D360_SIGMA_EPS) return trunc;
+        num = __dmul_rn(d, ndota);
+    }
+    double s0[VT], ss0[VT], rs0[VT];
+#pragma unroll
+    for (int v = 0; v < VT; ++v) s0[v] = ss0[v] = rs0[v] = 0.0;
+    bool bad = false;
+
+    const int half = (g.ns - 1) / 2;
+    const int st = g.stride;
+    int e_row = ce - half * st * (t.ww + 1);
+    for (int j = 0; j < g.ns; ++j) {
+        int e = e_row;
+        for (int i = 0; i < g.ns; ++i) {
+            const float4 q = t.qg[e];
+            double dn;
+            if constexpr (sizeof(HT) == 4) {
+                const float den = dot3_f32(nx, ny, nz, q.x, q.y, q.z);
+                bad = bad || (den > g.den_lim);
+                dn = (double)fminf(den, g.den_lim);
+            } else {
+                const double den = fma(nz, (double)q.z, fma(ny, (double)q.y, nx * (double)q.x));
+                const bool par = den > -D360_PARALLEL_EPS;
+                bad = bad || par;
+                dn = par ? -D360_PARALLEL_EPS : den;
+            }
+            const double lam = num * rcp3(dn);
+            const double rv = (double)q.w;
+            const double* rqe = t.rq + e;
+#pragma unroll
+            for (int v = 0; v < VT; ++v) {
+                const double tx = fma(lam, rqe[(v * 3 + 0) * t.ne], g.rel_t[v][0]);
+                const double ty = fma(lam, rqe[(v * 3 + 1) * t.ne], g.rel_t[v][1]);
+                const double tz = fma(lam, rqe[(v * 3 + 2) * t.ne], g.rel_t[v][2]);
+                float pu, pv;
+                project(g, tx, ty, tz, pu, pv);
+                const double val = (double)bilinear(g.nb + v * g.plane, g, pu, pv);
+                s0[v] += val;
+                ss0[v] = fma(val, val, ss0[v]);
+                rs0[v] = fma(rv, val, rs0[v]);
+            }
+            e += st;
+        }
+        e_row += st * t.ww;
+    }
+    if (bad) return trunc;
+
+    const double inv_s = g.inv_s;
+    double cv[VT];
+#pragma unroll
+    for (int v = 0; v < VT; ++v) {
+        cv[v] = trunc;
+        const double m0 = s0[v] * inv_s;
+        const double v0 = ss0[v] * inv_s - m0 * m0;
+        if (!(v0 < D360_VAR_EPS)) {
+            const double cov = rs0[v] * inv_s - mr * m0;
+            double c = 1.0 - cov / (sr * sqrt(v0));
+            c = c < 0.0 ? 0.0 : c;
+            c = c > trunc ? trunc : c;
+            cv[v] = c;
+        }
+    }
+    const double total = aggregate<VT>(cv, g.top_k);
+    return total == total ? total : trunc;  // NaN only from the unguarded polar singularities
+}
+
+// ---------------------------------------------------------------------------------------
+// eval_costs, K:300-349
+// ---------------------------------------------------------------------------------------
+template <int VT>
+__global__ void __launch_bounds__(THREADS, D360_FAST_MINB)
+    k_eval(const __grid_constant__ FastGroup g, const float* __restrict__ depth, const float* __restrict__ normal,
+           float* __restrict__ cost_out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH_FULL;
+    const Tile t = tile_setup<VT>(g, smem, x0, y0, TH_FULL);
+    __syncthreads();
+    const int lx = threadIdx.x % TW, ly = threadIdx.x / TW;
+    const int x = x0 + lx, y = y0 + ly;
+    if (x >= g.W || y >= g.H) return;
+    const int ce = (ly + g.reach) * t.ww + lx + g.reach;
+    double mr, sr;
+    pixel_stats(g, t, ce, mr, sr);
+    const size_t i = (size_t)y * g.W + x;
+    cost_out[i] = (float)cand_cost<VT, float>(g, t, ce, mr, sr, depth[i], normal[3 * i], normal[3 * i + 1],
+                                              normal[3 * i + 2]);
+}
+
+// ---------------------------------------------------------------------------------------
+// red_black_pass, K:352-473.  A CTA covers TW x TH_RB pixels; each of its 256 threads owns one
+// pixel of the requested colour and carries its off-colour neighbour over unchanged.
+// ---------------------------------------------------------------------------------------
+__constant__ int c_nbr2[8][2] = {{-1, -1}, {1, -1}, {-1, 1}, {1, 1}, {0, -2}, {0, 2}, {-2, 0}, {2, 0}};
+
+template <int VT>
+__global__ void __launch_bounds__(THREADS, D360_FAST_MINB)
+    k_red_black(const __grid_constant__ FastGroup g, int parity, const float* __restrict__ depth_in,
+                const float* __restrict__ normal_in, const float* __restrict__ cost_in, float* __restrict__ depth_out,
+                float* __restrict__ normal_out, float* __restrict__ cost_out, unsigned long long* n_evals) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH_RB;
+    const Tile t = tile_setup<VT>(g, smem, x0, y0, TH_RB);
+    __syncthreads();
+    const int ly = threadIdx.x / (TW / 2);
+    const int y = y0 + ly;
+    const int lx = 2 * (threadIdx.x % (TW / 2)) + ((parity + y) & 1);  // x0 is even
+    const int x = x0 + lx;
+    unsigned int evals = 0;
+    if (y < g.H) {
+        const int xo = x0 + (lx ^ 1);
+        if (xo < g.W) {
+            const size_t o = (size_t)y * g.W + xo;
+            depth_out[o] = depth_in[o];
+            normal_out[3 * o] = normal_in[3 * o];
+            normal_out[3 * o + 1] = normal_in[3 * o + 1];
+            normal_out[3 * o + 2] = normal_in[3 * o + 2];
+            cost_out[o] = cost_in[o];
+        }
+    }
+    if (x < g.W && y < g.H) {
+        const size_t i = (size_t)y * g.W + x;
+        float bd = depth_in[i];
+        float bnx = normal_in[3 * i], bny = normal_in[3 * i + 1], bnz = normal_in[3 * i + 2];
+        double bc = (double)cost_in[i];
+        const int ce = (ly + g.reach) * t.ww + lx + g.reach;
+        double mr = 0.0, sr = 0.0;
+        bool gathered = false;
+        float cd[8], cx[8], cy[8], cz[8];
+        int n_seen = 0;
+#pragma unroll 1
+        for (int j = 0; j < 8; ++j) {
+            const int qy = y + c_nbr2[j][1];
+            if (qy < 0 || qy >= g.H) continue;
+            const int qx = wrap_once(x + c_nbr2[j][0], g.W);
+            const size_t qi = (size_t)qy * g.W + qx;
+            const float d = depth_in[qi];
+            const float nx = normal_in[3 * qi], ny = normal_in[3 * qi + 1], nz = normal_in[3 * qi + 2];
+            bool dup = d == bd && nx == bnx && ny == bny && nz == bnz;
+#pragma unroll
+            for (int m = 0; m < 8; ++m)
+                if (m < n_seen) dup = dup || (d == cd[m] && nx == cx[m] && ny == cy[m] && nz == cz[m]);
+            if (dup) continue;
+#pragma unroll
+            for (int m = 0; m < 8; ++m)
+                if (m == n_seen) { cd[m] = d; cx[m] = nx; cy[m] = ny; cz[m] = nz; }
+            ++n_seen;
+            if (!gathered) {
+                pixel_stats(g, t, ce, mr, sr);
+                gathered = true;
+            }
+            const double c = cand_cost<VT, float>(g, t, ce, mr, sr, d, nx, ny, nz);
+            ++evals;
+            if (c < bc) {
+                bc = c;
+                bd = d; bnx = nx; bny = ny; bnz = nz;
+            }
+        }
+        depth_out[i] = bd;
+        normal_out[3 * i] = bnx;
+        normal_out[3 * i + 1] = bny;
+        normal_out[3 * i + 2] = bnz;
+        cost_out[i] = (float)bc;
+    }
+    if (n_evals != nullptr) {
+        for (int o = 16; o > 0; o >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, o);
+        if ((threadIdx.x & 31) == 0 && evals) atomicAdd(n_evals, (unsigned long long)evals);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// refine_pass, K:476-610.  Loop-carried d, n, c are f64 as in the reference.
+// ---------------------------------------------------------------------------------------
+template <int VT>
+__global__ void __launch_bounds__(THREADS, D360_FAST_MINB)
+    k_refine(const __grid_constant__ FastGroup g, const __grid_constant__ RefineTable tab, float* __restrict__ depth,
+             float* __restrict__ normal, float* __restrict__ cost, unsigned long long* n_evals) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH_FULL;
+    const Tile t = tile_setup<VT>(g, smem, x0, y0, TH_FULL);
+    __syncthreads();
+    const int lx = threadIdx.x % TW, ly = threadIdx.x / TW;
+    const int x = x0 + lx, y = y0 + ly;
+    unsigned int evals = 0;
+    if (x < g.W && y < g.H) {
+        const int ce = (ly + g.reach) * t.ww + lx + g.reach;
+        const size_t i = (size_t)y * g.W + x;
+        double d = depth[i];
+        double nx = normal[3 * i], ny = normal[3 * i + 1], nz = normal[3 * i + 2];
+        double c = cost[i];
+        const float4 a4 = t.qg[ce];
+        const double ax = a4.x, ay = a4.y, az = a4.z;
+        double mr, sr;
+        pixel_stats(g, t, ce, mr, sr);
+        bool stale = true;
+        double e1x = 0, e1y = 0, e1z = 0, e2x = 0, e2y = 0, e2z = 0;
+#pragma unroll 1
+        for (int k = 0; k < tab.n; ++k) {
+            double nd = __dadd_rn(d, (double)tab.dd[k]);
+            if (nd < tab.depth_min) nd = tab.depth_min;
+            else if (nd > tab.depth_max) nd = tab.depth_max;
+            if (stale) {
+                e1x = __dsub_rn(__dmul_rn(ny, az), __dmul_rn(nz, ay));
+                e1y = __dsub_rn(__dmul_rn(nz, ax), __dmul_rn(nx, az));
+                e1z = __dsub_rn(__dmul_rn(nx, ay), __dmul_rn(ny, ax));
+                double m2 = dot3_f64(e1x, e1y, e1z, e1x, e1y, e1z);
+                if (m2 < 1e-12) {
+                    e1x = -nz; e1y = 0.0; e1z = nx;
+                    m2 = __dadd_rn(__dmul_rn(e1x, e1x), __dmul_rn(e1z, e1z));
+                    if (m2 < 1e-12) { e1x = 1.0; e1z = 0.0; m2 = 1.0; }
+                }
+                const double inv = 1.0 / sqrt(m2);
+                e1x = __dmul_rn(e1x, inv); e1y = __dmul_rn(e1y, inv); e1z = __dmul_rn(e1z, inv);
+                e2x = __dsub_rn(__dmul_rn(ny, e1z), __dmul_rn(nz, e1y));
+                e2y = __dsub_rn(__dmul_rn(nz, e1x), __dmul_rn(nx, e1z));
+                e2z = __dsub_rn(__dmul_rn(nx, e1y), __dmul_rn(ny, e1x));
+                stale = false;
+            }
+            const double sa = tab.sa[k], ca = tab.ca[k], caz = tab.caz[k], saz = tab.saz[k];
+            double cnx = __dadd_rn(__dmul_rn(nx, ca), __dmul_rn(__dadd_rn(__dmul_rn(e1x, caz), __dmul_rn(e2x, saz)), sa));
+            double cny = __dadd_rn(__dmul_rn(ny, ca), __dmul_rn(__dadd_rn(__dmul_rn(e1y, caz), __dmul_rn(e2y, saz)), sa));
+            double cnz = __dadd_rn(__dmul_rn(nz, ca), __dmul_rn(__dadd_rn(__dmul_rn(e1z, caz), __dmul_rn(e2z, saz)), sa));
+            const double nrm = sqrt(dot3_f64(cnx, cny, cnz, cnx, cny, cnz));
+            if (nrm < 1e-12) continue;
+            const double inv = 1.0 / nrm;
+            cnx = __dmul_rn(cnx, inv); cny = __dmul_rn(cny, inv); cnz = __dmul_rn(cnz, inv);
+            const double ev = cand_cost<VT, double>(g, t, ce, mr, sr, nd, cnx, cny, cnz);
+            ++evals;
+            if (ev < c) {
+                c = ev; d = nd; nx = cnx; ny = cny; nz = cnz;
+                stale = true;
+            }
+        }
+        depth[i] = (float)d;
+        normal[3 * i] = (float)nx;
+        normal[3 * i + 1] = (float)ny;
+        normal[3 * i + 2] = (float)nz;
+        cost[i] = (float)c;
+    }
+    if (n_evals != nullptr) {
+        for (int o = 16; o > 0; o >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, o);
+        if ((threadIdx.x & 31) == 0 && evals) atomicAdd(n_evals, (unsigned long long)evals);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------------------
+static bool make_fast_group(const GroupDev& gd, FastGroup* out) {
+    // regular grid?  S = ns^2, offsets (dx, dy) = stride * (i - half, j - half), dy outer (E:60-65)
+    int ns = 1;
+    while (ns * ns < gd.S) ++ns;
+    if (ns * ns != gd.S || (ns & 1) == 0) return false;
+    const int half = (ns - 1) / 2;
+    const int stride = ns > 1 ? gd.dx[1] - gd.dx[0] : 1;
+    if (stride < 1) return false;
+    for (int k = 0; k < gd.S; ++k) {
+        if (gd.dx[k] != (k % ns - half) * stride || gd.dy[k] != (k / ns - half) * stride) return false;
+    }
+    if (gd.nb_pad_x < 1 || gd.nb_pad_y < 1) return false;  // needs the padded neighbour planes
+    const long long pitch = gd.W + 2 * gd.nb_pad_x, rows = gd.H + 2 * gd.nb_pad_y;
+    if (pitch * rows >= (1ll << 23)) return false;  // f32 index arithmetic must stay exact
+    FastGroup& g = *out;
+    g.W = gd.W; g.H = gd.H; g.ns = ns; g.stride = stride; g.reach = half * stride; g.top_k = gd.top_k;
+    g.pitch = (int)pitch;
+    g.plane = (size_t)(pitch * rows);
+    g.max_idx = (unsigned)(pitch * rows - pitch - 2);
+    g.pitch_f = (float)pitch;
+    g.idx_bias = 8388608.0f + (float)(gd.nb_pad_y * pitch + gd.nb_pad_x);
+    g.rays = gd.rays; g.ref_gray = gd.ref_gray; g.nb = gd.nb;
+    for (int v = 0; v < gd.V; ++v) {
+        for (int i = 0; i < 9; ++i) g.rel_r[v][i] = gd.rel_r[v][i];
+        for (int i = 0; i < 3; ++i) g.rel_t[v][i] = (double)gd.rel_t[v][i];
+    }
+    const double hw = gd.W * (0.5 / D360_PI), ls = gd.H / D360_PI;
+    for (int oct = 0; oct < 8; ++oct) {
+        const bool swap = oct & 1, xneg = oct & 2, yneg = oct & 4;
+        // theta = sy * (cx + sx * (cs + ss * p)), K:96-99
+        const double ss = swap ? -1.0 : 1.0, cs = swap ? D360_HALF_PI : 0.0;
+        const double sx = xneg ? -1.0 : 1.0, cx = xneg ? D360_PI : 0.0;
+        const double sy = yneg ? -1.0 : 1.0;
+        g.mu[oct] = sy * sx * ss * hw;
+        g.cu[oct] = (sy * (cx + sx * cs) + D360_PI) * hw - 0.5;
+    }
+    g.mv[0] = ls;  g.cv[0] = -0.5;                  // ty < 0: sphi > 0
+    g.mv[1] = -ls; g.cv[1] = D360_PI * ls - 0.5;    // ty > 0: sphi < 0, acos = pi - p (K:131)
+    static const double CA[8] = {-5.021063913876e-03, 2.533170107199e-02, -6.087448223083e-02, 1.000220525649e-01,
+                                 -1.404782123164e-01, 1.997402857787e-01, -3.333223261885e-01, 9.999999227776e-01};
+    static const double CQ[8] = {-1.223553911532e-03, 6.510368059701e-03, -1.682974898800e-02, 3.068214201158e-02,
+                                 -5.008467775423e-02, 8.895977933699e-02, -2.145970563340e-01, 1.570796263346e00};
+    for (int i = 0; i < 8; ++i) { g.ca[i] = CA[i]; g.cq[i] = CQ[i]; }
+    g.trunc = gd.trunc;
+    g.inv_s = 1.0 / gd.S;
+    g.den_lim = nextafterf((float)(-D360_PARALLEL_EPS), -1.0f);
+    if ((double)g.den_lim >= -D360_PARALLEL_EPS) g.den_lim = nextafterf(g.den_lim, -1.0f);
+    return true;
+}
+
+template <typename K>
+static int prepare(K kernel, size_t smem) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) {
+        set_error("cudaFuncSetAttribute(%zu B smem): %s", smem, cudaGetErrorString(e));
+        return 1;
+    }
+    return 0;
+}
+
+#define D360_FAST_DISPATCH(V, ...)                             \
+    switch (V) {                                                \
+        case 1: { constexpr int VT = 1; __VA_ARGS__; } break;   \
+        case 2: { constexpr int VT = 2; __VA_ARGS__; } break;   \
+        case 3: { constexpr int VT = 3; __VA_ARGS__; } break;   \
+        case 4: { constexpr int VT = 4; __VA_ARGS__; } break;   \
+        case 6: { constexpr int VT = 6; __VA_ARGS__; } break;   \
+        default: return -1;                                     \
+    }
+
+}  // namespace fast
+
+using namespace fast;
+
+// Each returns -1 when the fast path does not apply (caller falls back to the generic kernel).
+int fast_eval(const GroupDev& gd, const float* depth, const float* normal, float* cost_out, cudaStream_t s) {
+    FastGroup g;
+    if (!make_fast_group(gd, &g)) return -1;
+    const size_t smem = tile_bytes(TW, TH_FULL, g.reach, gd.V);
+    if (smem > 200 * 1024) return -1;
+    dim3 grid((gd.W + TW - 1) / TW, (gd.H + TH_FULL - 1) / TH_FULL);
+    D360_FAST_DISPATCH(gd.V, {
+        auto k = k_eval<VT>;
+        if (prepare(k, smem)) return 1;
+        TraceScope ts_("eval_costs", s);
+        k<<<grid, THREADS, smem, s>>>(g, depth, normal, cost_out);
+    })
+    return check_launch("eval_costs");
+}
+
+int fast_red_black(const GroupDev& gd, int parity, const float* di, const float* ni, const float* ci, float* dout,
+                   float* nout, float* cout, unsigned long long* n_evals, cudaStream_t s) {
+    FastGroup g;
+    if (!make_fast_group(gd, &g)) return -1;
+    const size_t smem = tile_bytes(TW, TH_RB, g.reach, gd.V);
+    if (smem > 200 * 1024) return -1;
+    dim3 grid((gd.W + TW - 1) / TW, (gd.H + TH_RB - 1) / TH_RB);
+    D360_FAST_DISPATCH(gd.V, {
+        auto k = k_red_black<VT>;
+        if (prepare(k, smem)) return 1;
+        TraceScope ts_("red_black", s);
+        k<<<grid, THREADS, smem, s>>>(g, parity, di, ni, ci, dout, nout, cout, n_evals);
+    })
+    return check_launch("red_black_pass");
+}
+
+int fast_refine(const GroupDev& gd, const RefineTable& tab, float* depth, float* normal, float* cost,
+                unsigned long long* n_evals, cudaStream_t s) {
+    FastGroup g;
+    if (!make_fast_group(gd, &g)) return -1;
+    const size_t smem = tile_bytes(TW, TH_FULL, g.reach, gd.V);
+    if (smem > 200 * 1024) return -1;
+    dim3 grid((gd.W + TW - 1) / TW, (gd.H + TH_FULL - 1) / TH_FULL);
+    D360_FAST_DISPATCH(gd.V, {
+        auto k = k_refine<VT>;
+        if (prepare(k, smem)) return 1;
+        TraceScope ts_("refine", s);
+        k<<<grid, THREADS, smem, s>>>(g, tab, depth, normal, cost, n_evals);
+    })
+    return check_launch("refine_pass");
+}
+
+}  // namespace d360

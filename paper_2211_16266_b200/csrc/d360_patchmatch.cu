@@ -82,7 +82,7 @@ __device__ __forceinline__ void pixel_stats(const GroupDev& g, const Tile& t, in
 
 // K:134-153 on the f32-rounded projection.  EXACT: f64 weights like the reference.
 template <int MODE>
-__device__ __forceinline__ double bilinear(const float* __restrict__ img, int H, int W, float u,
+__device__ __forceinline__ double bilinear(const float* __restrict__ img, int H, int W, int pitch, float u,
                                            float v) {
     const float fl = floorf(u);
     int u0 = (int)fl;
@@ -97,8 +97,8 @@ __device__ __forceinline__ double bilinear(const float* __restrict__ img, int H,
     int v0 = (int)vc;
     v0 = v0 > H - 2 ? H - 2 : v0;
     v0 = max(v0, 0);
-    const float* r0 = img + (size_t)v0 * W;
-    const float* r1 = r0 + W;
+    const float* r0 = img + (size_t)v0 * pitch;
+    const float* r1 = r0 + pitch;
     const float a = __ldg(r0 + u0), b = __ldg(r0 + u1), c = __ldg(r1 + u0), d = __ldg(r1 + u1);
     if constexpr (MODE == D360_PREC_EXACT) {
         const double fu = (double)u - (double)fl;
@@ -158,7 +158,9 @@ __device__ __forceinline__ double cand_cost(const GroupDev& g, const Tile& t, in
     const double half_w = g.W * (0.5 / D360_PI);
     const double lat_scale = g.H / D360_PI;
     const int H = g.H, W = g.W;
-    const size_t plane = (size_t)H * W;
+    const int pitch = W + 2 * g.nb_pad_x;
+    const size_t plane = (size_t)(H + 2 * g.nb_pad_y) * pitch;
+    const float* nb0 = g.nb + (size_t)g.nb_pad_y * pitch + g.nb_pad_x;  // pixel (0, 0) of view 0
 
     double s0[NV], ss0[NV], rs0[NV];
 #pragma unroll
@@ -191,7 +193,7 @@ __device__ __forceinline__ double cand_cost(const GroupDev& g, const Tile& t, in
                 const float pu =
                     (float)madd<MODE>(__dadd_rn(fast_atan2<MODE>(tx, tz), D360_PI), half_w, -0.5);
                 const float pv = (float)madd<MODE>(fast_acos<MODE>(sphi), lat_scale, -0.5);
-                const double val = bilinear<MODE>(g.nb + v * plane, H, W, pu, pv);
+                const double val = bilinear<MODE>(nb0 + v * plane, H, W, pitch, pu, pv);
                 s0[v] = __dadd_rn(s0[v], val);
                 ss0[v] = madd<MODE>(val, val, ss0[v]);
                 rs0[v] = madd<MODE>(rv, val, rs0[v]);
@@ -331,13 +333,6 @@ __global__ void __launch_bounds__(RB_THREADS)
 // ---------------------------------------------------------------------------------------
 // refine_pass, K:476-610.  Loop-carried d, n, c are f64 as in the reference.
 // ---------------------------------------------------------------------------------------
-struct RefineTable {
-    float dd[D360_MAX_REFINE], sa[D360_MAX_REFINE], ca[D360_MAX_REFINE], caz[D360_MAX_REFINE],
-        saz[D360_MAX_REFINE];
-    int n;
-    double depth_min, depth_max;
-};
-
 template <int MODE, int VT>
 __global__ void __launch_bounds__(TILE_W* TILE_H)
     k_refine(const __grid_constant__ GroupDev g, const __grid_constant__ RefineTable tab,
@@ -446,6 +441,10 @@ static int prepare_kernel(K kernel, size_t smem) {
 
 static int launch_eval(const GroupDev& gd, int prec, const float* depth, const float* normal,
                        float* cost_out, cudaStream_t s) {
+    if (prec == D360_PREC_MIXED) {
+        const int frc = fast_eval(gd, depth, normal, cost_out, s);
+        if (frc >= 0) return frc;
+    }
     const size_t smem = tile_smem_bytes(TILE_W, TILE_H, gd.reach, gd.V);
     dim3 grid((gd.W + TILE_W - 1) / TILE_W, (gd.H + TILE_H - 1) / TILE_H);
     int rc = 0;
@@ -463,6 +462,10 @@ static int launch_eval(const GroupDev& gd, int prec, const float* depth, const f
 static int launch_red_black(const GroupDev& gd, int prec, int parity, const float* di,
                             const float* ni, const float* ci, float* dout, float* nout, float* cout,
                             unsigned long long* n_evals, cudaStream_t s) {
+    if (prec == D360_PREC_MIXED) {
+        const int frc = fast_red_black(gd, parity, di, ni, ci, dout, nout, cout, n_evals, s);
+        if (frc >= 0) return frc;
+    }
     const size_t smem = tile_smem_bytes(TILE_W, TILE_H, gd.reach, gd.V);
     dim3 grid((gd.W + TILE_W - 1) / TILE_W, (gd.H + TILE_H - 1) / TILE_H);
     int rc = 0;
@@ -479,6 +482,10 @@ static int launch_red_black(const GroupDev& gd, int prec, int parity, const floa
 
 static int launch_refine(const GroupDev& gd, int prec, const RefineTable& tab, float* depth,
                          float* normal, float* cost, unsigned long long* n_evals, cudaStream_t s) {
+    if (prec == D360_PREC_MIXED) {
+        const int frc = fast_refine(gd, tab, depth, normal, cost, n_evals, s);
+        if (frc >= 0) return frc;
+    }
     const size_t smem = tile_smem_bytes(TILE_W, TILE_H, gd.reach, gd.V);
     dim3 grid((gd.W + TILE_W - 1) / TILE_W, (gd.H + TILE_H - 1) / TILE_H);
     int rc = 0;

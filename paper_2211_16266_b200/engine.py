@@ -220,9 +220,17 @@ class DeviceDepthPanorama:
 # PreparedGroup (E:137-160): images -> luma on the device, rays, relative poses, offsets
 # ---------------------------------------------------------------------------------------
 
-def to_gray_device(image, device=None, out: torch.Tensor | None = None) -> torch.Tensor:
+NB_PAD_X = 4  # wrapped columns each side of a neighbour plane (keeps rows 16-byte aligned)
+NB_PAD_Y = 1  # replicated rows above / below
+
+
+def to_gray_device(image, device=None, out: torch.Tensor | None = None, pad=(0, 0)) -> torch.Tensor:
     """uint8 (H,W) / (H,W,3) numpy array or CUDA tensor -> float32 luma on the device
-    (keyframes.py:64-72, float32 arithmetic).  ``out``: optional contiguous (H,W) f32 target."""
+    (keyframes.py:64-72, float32 arithmetic).
+
+    ``pad=(px, py)`` writes the padded plane layout of ``d360_group.nb``: shape
+    (H + 2 py, W + 2 px) with wrapped columns and replicated rows.  ``out``: optional
+    contiguous float32 target of that shape."""
     dev = _device(device)
     lib = _lib.load()
     img = image if isinstance(image, torch.Tensor) else _up(np.asarray(image), np.uint8, dev)
@@ -236,11 +244,13 @@ def to_gray_device(image, device=None, out: torch.Tensor | None = None) -> torch
         raise ValueError(f"expected (H, W) or (H, W, 3) image, got {tuple(img.shape)}")
     img = img.contiguous()
     h, w = img.shape[:2]
+    px, py = int(pad[0]), int(pad[1])
+    shape = (h + 2 * py, w + 2 * px)
     if out is None:
-        out = torch.empty((h, w), dtype=torch.float32, device=dev)
-    elif out.shape != (h, w) or out.dtype != torch.float32 or not out.is_contiguous():
-        raise ValueError("out must be a contiguous float32 (H, W) tensor")
-    _lib.check(lib.d360_to_gray(_ptr(img), ch, _ptr(out), h, w, _stream()), "to_gray")
+        out = torch.empty(shape, dtype=torch.float32, device=dev)
+    elif tuple(out.shape) != shape or out.dtype != torch.float32 or not out.is_contiguous():
+        raise ValueError(f"out must be a contiguous float32 {shape} tensor")
+    _lib.check(lib.d360_to_gray_padded(_ptr(img), ch, _ptr(out), h, w, px, py, _stream()), "to_gray")
     return out
 
 
@@ -275,18 +285,26 @@ class PreparedGroup:
             ref_img = imgs[0] if isinstance(imgs[0], torch.Tensor) else _up(np.asarray(imgs[0]), np.uint8, self.device)
             self.ref_image = ref_img  # u8 (H,W) / (H,W,3) on the device; fusion reads its colours
             self.ref_gray = to_gray_device(ref_img, self.device)
-            self.nb = torch.empty((self.n_views, *self.camera.shape), dtype=torch.float32, device=self.device)
+            h, w = self.camera.shape
+            # neighbour luma planes, padded so that every bilinear footprint is in-plane (d360.h)
+            self.nb_padded = torch.empty((self.n_views, h + 2 * NB_PAD_Y, w + 2 * NB_PAD_X), dtype=torch.float32,
+                                         device=self.device)
             for v, im in enumerate(imgs[1:]):
-                to_gray_device(im, self.device, out=self.nb[v])
+                to_gray_device(im, self.device, out=self.nb_padded[v], pad=(NB_PAD_X, NB_PAD_Y))
         rel = [relative_transform(group.reference.pose, nb.pose) for nb in group.neighbors]
         self.rel_r = np.ascontiguousarray(np.stack([r for r, _ in rel]), dtype=np.float32)
         self.rel_t = np.ascontiguousarray(np.stack([t for _, t in rel]), dtype=np.float32)
         self._struct = _lib.Group(
             width=self.camera.width, height=self.camera.height, n_views=self.n_views,
             n_samples=len(self.offsets), top_k=self.top_k, precision=PRECISIONS[self.precision],
-            rays=_ptr(self.cam_dev.rays32), ref_gray=_ptr(self.ref_gray), nb=_ptr(self.nb),
+            rays=_ptr(self.cam_dev.rays32), ref_gray=_ptr(self.ref_gray), nb=_ptr(self.nb_padded), nb_pad_x=NB_PAD_X, nb_pad_y=NB_PAD_Y,
             rel_r=self.rel_r.ctypes.data, rel_t=self.rel_t.ctypes.data, offsets=self.offsets.ctypes.data,
             trunc=float(spec.cost_truncation))
+
+    @property
+    def nb(self) -> torch.Tensor:
+        """(V, H, W) view of the neighbour luma planes without the padding."""
+        return self.nb_padded[:, NB_PAD_Y:-NB_PAD_Y, NB_PAD_X:-NB_PAD_X]
 
     @property
     def struct(self):
