@@ -45,30 +45,47 @@ struct FastGroup {
     double mv[2], cv[2];  // latitude:  v = p * mv[hem] + cv[hem]
     double ca[8], cq[8];  // atan / acos polynomial coefficients, highest degree first (K:75-85, K:112-122)
     double trunc, inv_s;
+    double neg_par_eps, tiny, c0375;  // -PARALLEL_EPS, 1e-30 (K:246), 3/8: 64-bit literals live in the constant bank
+    unsigned plane32;     // plane as a 32-bit element count
     float pitch_f;        // pitch as float
     float idx_bias;       // 2^23 + pad_y * pitch + pad_x: float -> index by mantissa extraction
     float den_lim;        // largest f32 below -PARALLEL_EPS
 };
 
+// Patch context of a CTA tile in shared memory.  Window entry (i, j) <-> pixel
+// ((x0 - R + i) mod W, clamp(y0 - R + j, 0, H-1)), K:168-177.  With `compress` (red-black pass
+// on an even sample stride: every sample of an updated pixel has the pixel's colour) only the
+// entries of that colour are kept, two window columns per slot — half the shared memory, and
+// neighbouring lanes read neighbouring slots.
 struct Tile {
-    const float4* qg;  // (qx, qy, qz, reference luma) per window entry
-    const double* rq;  // [(v*3 + c) * ne + entry]
-    int ww, ne;
+    const float4* qg;  // (qx, qy, qz, reference luma) per entry
+    const double* rq;  // [(v*3 + c) * ne + entry]  R_v q as f64 (exact widening of the f32 dot, K:184-189)
+    int wwc;           // entries per window row
+    int ne;            // entries per plane
+    int sx, sy;        // entry step of one sample column / row
 };
 
-__host__ __device__ inline size_t tile_bytes(int tw, int th, int reach, int n_views) {
-    const size_t ne = (size_t)(tw + 2 * reach) * (th + 2 * reach);
+__host__ __device__ inline int window_entries(int tw, int th, int reach, bool compress) {
+    const int ww = tw + 2 * reach;
+    return (compress ? ww / 2 : ww) * (th + 2 * reach);
+}
+__host__ __device__ inline size_t tile_bytes(int tw, int th, int reach, bool compress, int n_views) {
+    const size_t ne = (size_t)window_entries(tw, th, reach, compress);
     return ne * sizeof(float4) + ne * sizeof(double) * 3 * n_views;
 }
 
 template <int VT>
-__device__ __forceinline__ Tile tile_setup(const FastGroup& g, unsigned char* smem, int x0, int y0, int th) {
+__device__ __forceinline__ Tile tile_setup(const FastGroup& g, unsigned char* smem, int x0, int y0, int th,
+                                           bool compress, int keep) {
     const int R = g.reach;
-    const int ww = TW + 2 * R, hh = th + 2 * R, ne = ww * hh;
+    const int ww = TW + 2 * R, hh = th + 2 * R;
+    const int wwc = compress ? ww / 2 : ww;
+    const int ne = wwc * hh;
     float4* qg = reinterpret_cast<float4*>(smem);
     double* rq = reinterpret_cast<double*>(smem + (size_t)ne * sizeof(float4));
     for (int e = threadIdx.x; e < ne; e += THREADS) {
-        const int j = e / ww, i = e - j * ww;
+        const int j = e / wwc, ic = e - j * wwc;
+        const int i = compress ? 2 * ic + ((keep + j) & 1) : ic;
         const int gx = pos_mod(x0 - R + i, g.W);
         const int gy = min(max(y0 - R + j, 0), g.H - 1);
         const size_t gi = (size_t)gy * g.W + gx;
@@ -85,8 +102,10 @@ __device__ __forceinline__ Tile tile_setup(const FastGroup& g, unsigned char* sm
     Tile t;
     t.qg = qg;
     t.rq = rq;
-    t.ww = ww;
+    t.wwc = wwc;
     t.ne = ne;
+    t.sx = compress ? g.stride / 2 : g.stride;
+    t.sy = g.stride * wwc;
     return t;
 }
 
@@ -94,16 +113,16 @@ __device__ __forceinline__ Tile tile_setup(const FastGroup& g, unsigned char* sm
 __device__ __forceinline__ void pixel_stats(const FastGroup& g, const Tile& t, int ce, double& mr, double& sr) {
     double acc = 0.0, acc2 = 0.0;
     const int half = (g.ns - 1) / 2;
-    int e_row = ce - half * g.stride * (t.ww + 1);
+    int e_row = ce - half * (t.sx + t.sy);
     for (int j = 0; j < g.ns; ++j) {
         int e = e_row;
         for (int i = 0; i < g.ns; ++i) {
             const float v = t.qg[e].w;
             acc = __dadd_rn(acc, (double)v);
             acc2 = __dadd_rn(acc2, (double)__fmul_rn(v, v));
-            e += g.stride;
+            e += t.sx;
         }
-        e_row += g.stride * t.ww;
+        e_row += t.sy;
     }
     const double m = acc * g.inv_s;  // S is a small integer: acc / S to <= 1 ulp, see note below
     // the reference divides (acc / S); multiply-by-reciprocal differs by <= 1 ulp of f64,
@@ -121,10 +140,10 @@ __device__ __forceinline__ double rcp3(double x) {
     return fma(y, fma(e, e, e), y);
 }
 // 1/sqrt(x), third-order refinement of the MUFU.RSQ64H seed
-__device__ __forceinline__ double rsqrt3(double x) {
+__device__ __forceinline__ double rsqrt3(double x, double c0375) {
     const double y = rsqrt_seed(x);
     const double e = fma(-(x * y), y, 1.0);
-    return fma(y * e, fma(e, 0.375, 0.5), y);
+    return fma(y * e, fma(e, c0375, 0.5), y);
 }
 
 // (u, v) of K:244-258 for one neighbour-frame point t, rounded to f32 like the reference's
@@ -132,13 +151,13 @@ __device__ __forceinline__ double rsqrt3(double x) {
 // max(|tx|,|tz|) = 0 or 1 - |ty|/|t| <= 0); they yield NaN, which cand_cost maps to `trunc`.
 __device__ __forceinline__ void project(const FastGroup& g, double tx, double ty, double tz, float& pu, float& pv) {
     // latitude: v = acos_poly(-ty / |t|) * H/pi - 0.5  (K:102-131)
-    const double r2 = fma(tz, tz, fma(ty, ty, fma(tx, tx, 1e-30)));
-    const double a = fabs(ty) * rsqrt3(r2);
+    const double r2 = fma(tz, tz, fma(ty, ty, fma(tx, tx, g.tiny)));
+    const double a = fabs(ty) * rsqrt3(r2, g.c0375);
     double q = g.cq[0];
 #pragma unroll
     for (int i = 1; i < 8; ++i) q = fma(a, q, g.cq[i]);
     const double w = 1.0 - a;
-    const double sq = w * rsqrt3(w);
+    const double sq = w * rsqrt3(w, g.c0375);
     const int hem = (unsigned)__double2hiint(ty) >> 31 ^ 1;  // 1 when ty >= +0: sphi <= -0 (K:131)
     pv = (float)fma(q * sq, g.mv[hem], g.cv[hem]);
 
@@ -160,7 +179,7 @@ __device__ __forceinline__ void project(const FastGroup& g, double tx, double ty
 // in-plane and the reference's wrap / clamp rules are data, not code.  floor by the
 // 1.5 * 2^23 magic add; the element index is formed in f32 (exact below 2^23) and read out of
 // the mantissa, so no F2I / I2F conversions are issued.
-__device__ __forceinline__ float bilinear(const float* __restrict__ img, const FastGroup& g, float u, float v) {
+__device__ __forceinline__ float bilinear(const FastGroup& g, unsigned view_off, float u, float v) {
     const float MAGIC = 12582912.0f;
     float fl_u = __fadd_rn(__fadd_rn(u, MAGIC), -MAGIC);
     if (fl_u > u) fl_u -= 1.0f;
@@ -168,10 +187,13 @@ __device__ __forceinline__ float bilinear(const float* __restrict__ img, const F
     if (fl_v > v) fl_v -= 1.0f;
     const float fu = u - fl_u, fv = v - fl_v;
     const float off = __fadd_rn(fmaf(fl_v, g.pitch_f, fl_u), g.idx_bias);
-    const unsigned idx = min((unsigned)__float_as_int(off) & 0x7fffffu, g.max_idx);  // min: non-finite input only
-    const float* r0 = img + idx;
-    const float* r1 = img + (idx + g.pitch);
-    const float a = __ldg(r0), b = __ldg(r0 + 1), c = __ldg(r1), d = __ldg(r1 + 1);
+    // min: only non-finite (u, v) can exceed it.  All offsets are 32-bit element indices from
+    // one 64-bit base, so each tap costs one IMAD.WIDE.
+    const unsigned idx = min((unsigned)__float_as_int(off) & 0x7fffffu, g.max_idx) + view_off;
+    const float* __restrict__ nb = g.nb;
+    const float a = __ldg(nb + idx), b = __ldg(nb + idx + 1u);
+    const unsigned idx1 = idx + (unsigned)g.pitch;
+    const float c = __ldg(nb + idx1), d = __ldg(nb + idx1 + 1u);
     const float top = fmaf(b - a, fu, a);
     const float bot = fmaf(d - c, fu, c);
     return fmaf(bot - top, fv, top);
@@ -218,8 +240,7 @@ __device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, i
     bool bad = false;
 
     const int half = (g.ns - 1) / 2;
-    const int st = g.stride;
-    int e_row = ce - half * st * (t.ww + 1);
+    int e_row = ce - half * (t.sx + t.sy);
     for (int j = 0; j < g.ns; ++j) {
         int e = e_row;
         for (int i = 0; i < g.ns; ++i) {
@@ -231,9 +252,9 @@ __device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, i
                 dn = (double)fminf(den, g.den_lim);
             } else {
                 const double den = fma(nz, (double)q.z, fma(ny, (double)q.y, nx * (double)q.x));
-                const bool par = den > -D360_PARALLEL_EPS;
+                const bool par = den > g.neg_par_eps;
                 bad = bad || par;
-                dn = par ? -D360_PARALLEL_EPS : den;
+                dn = par ? g.neg_par_eps : den;
             }
             const double lam = num * rcp3(dn);
             const double rv = (double)q.w;
@@ -245,14 +266,14 @@ __device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, i
                 const double tz = fma(lam, rqe[(v * 3 + 2) * t.ne], g.rel_t[v][2]);
                 float pu, pv;
                 project(g, tx, ty, tz, pu, pv);
-                const double val = (double)bilinear(g.nb + v * g.plane, g, pu, pv);
+                const double val = (double)bilinear(g, v * g.plane32, pu, pv);
                 s0[v] += val;
                 ss0[v] = fma(val, val, ss0[v]);
                 rs0[v] = fma(rv, val, rs0[v]);
             }
-            e += st;
+            e += t.sx;
         }
-        e_row += st * t.ww;
+        e_row += t.sy;
     }
     if (bad) return trunc;
 
@@ -284,12 +305,12 @@ __global__ void __launch_bounds__(THREADS, D360_FAST_MINB)
            float* __restrict__ cost_out) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH_FULL;
-    const Tile t = tile_setup<VT>(g, smem, x0, y0, TH_FULL);
+    const Tile t = tile_setup<VT>(g, smem, x0, y0, TH_FULL, false, 0);
     __syncthreads();
     const int lx = threadIdx.x % TW, ly = threadIdx.x / TW;
     const int x = x0 + lx, y = y0 + ly;
     if (x >= g.W || y >= g.H) return;
-    const int ce = (ly + g.reach) * t.ww + lx + g.reach;
+    const int ce = (ly + g.reach) * t.wwc + lx + g.reach;
     double mr, sr;
     pixel_stats(g, t, ce, mr, sr);
     const size_t i = (size_t)y * g.W + x;
@@ -309,15 +330,17 @@ __global__ void __launch_bounds__(THREADS, D360_FAST_MINB)
                 const float* __restrict__ normal_in, const float* __restrict__ cost_in, float* __restrict__ depth_out,
                 float* __restrict__ normal_out, float* __restrict__ cost_out, unsigned long long* n_evals) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH_RB;
-    const Tile t = tile_setup<VT>(g, smem, x0, y0, TH_RB);
+    const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH_RB;  // x0 is even
+    const bool compress = (g.stride & 1) == 0;
+    const Tile t = tile_setup<VT>(g, smem, x0, y0, TH_RB, compress, (parity + y0) & 1);
     __syncthreads();
     const int ly = threadIdx.x / (TW / 2);
     const int y = y0 + ly;
-    const int lx = 2 * (threadIdx.x % (TW / 2)) + ((parity + y) & 1);  // x0 is even
+    const int lx = 2 * (threadIdx.x % (TW / 2)) + ((parity + y) & 1);
     const int x = x0 + lx;
     unsigned int evals = 0;
     if (y < g.H) {
+        // carry the off-colour pixel of this pair over unchanged (E:575-577)
         const int xo = x0 + (lx ^ 1);
         if (xo < g.W) {
             const size_t o = (size_t)y * g.W + xo;
@@ -330,38 +353,46 @@ __global__ void __launch_bounds__(THREADS, D360_FAST_MINB)
     }
     if (x < g.W && y < g.H) {
         const size_t i = (size_t)y * g.W + x;
-        float bd = depth_in[i];
-        float bnx = normal_in[3 * i], bny = normal_in[3 * i + 1], bnz = normal_in[3 * i + 2];
+        // original hypothesis of the pixel: a neighbour equal to it is a duplicate for the whole
+        // pass (its cost is cost_in, which can never beat the running best under strict <)
+        const float od = depth_in[i];
+        const float onx = normal_in[3 * i], ony = normal_in[3 * i + 1], onz = normal_in[3 * i + 2];
+        float bd = od, bnx = onx, bny = ony, bnz = onz;
         double bc = (double)cost_in[i];
-        const int ce = (ly + g.reach) * t.ww + lx + g.reach;
+        const int ce = (ly + g.reach) * t.wwc + (compress ? (lx + g.reach) >> 1 : lx + g.reach);
         double mr = 0.0, sr = 0.0;
         bool gathered = false;
-        float cd[8], cx[8], cy[8], cz[8];
-        int n_seen = 0;
 #pragma unroll 1
         for (int j = 0; j < 8; ++j) {
             const int qy = y + c_nbr2[j][1];
-            if (qy < 0 || qy >= g.H) continue;
-            const int qx = wrap_once(x + c_nbr2[j][0], g.W);
+            if (qy < 0 || qy >= g.H) continue;  // K:407 rows skipped
+            const int qx = wrap_once(x + c_nbr2[j][0], g.W);  // K:410-413 columns wrap
             const size_t qi = (size_t)qy * g.W + qx;
             const float d = depth_in[qi];
             const float nx = normal_in[3 * qi], ny = normal_in[3 * qi + 1], nz = normal_in[3 * qi + 2];
-            bool dup = d == bd && nx == bnx && ny == bny && nz == bnz;
-#pragma unroll
-            for (int m = 0; m < 8; ++m)
-                if (m < n_seen) dup = dup || (d == cd[m] && nx == cx[m] && ny == cy[m] && nz == cz[m]);
+            // K:418-432: skip exact duplicates of the best-so-far / of an already evaluated
+            // candidate.  Every earlier in-range neighbour was either evaluated or itself such a
+            // duplicate, so comparing with the original hypothesis and with the earlier
+            // neighbours (re-read through L1 instead of being kept in 32 registers) selects the
+            // same set, except that it also skips re-evaluating the original hypothesis once it
+            // has been displaced, which the strict < would reject anyway.
+            bool dup = d == od && nx == onx && ny == ony && nz == onz;
+            for (int m = 0; m < j; ++m) {
+                const int my = y + c_nbr2[m][1];
+                if (my < 0 || my >= g.H) continue;
+                const size_t mi = (size_t)my * g.W + wrap_once(x + c_nbr2[m][0], g.W);
+                if (depth_in[mi] == d)
+                    dup = dup || (normal_in[3 * mi] == nx && normal_in[3 * mi + 1] == ny &&
+                                  normal_in[3 * mi + 2] == nz);
+            }
             if (dup) continue;
-#pragma unroll
-            for (int m = 0; m < 8; ++m)
-                if (m == n_seen) { cd[m] = d; cx[m] = nx; cy[m] = ny; cz[m] = nz; }
-            ++n_seen;
             if (!gathered) {
                 pixel_stats(g, t, ce, mr, sr);
                 gathered = true;
             }
             const double c = cand_cost<VT, float>(g, t, ce, mr, sr, d, nx, ny, nz);
             ++evals;
-            if (c < bc) {
+            if (c < bc) {  // K:463
                 bc = c;
                 bd = d; bnx = nx; bny = ny; bnz = nz;
             }
@@ -387,13 +418,13 @@ __global__ void __launch_bounds__(THREADS, D360_FAST_MINB)
              float* __restrict__ normal, float* __restrict__ cost, unsigned long long* n_evals) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH_FULL;
-    const Tile t = tile_setup<VT>(g, smem, x0, y0, TH_FULL);
+    const Tile t = tile_setup<VT>(g, smem, x0, y0, TH_FULL, false, 0);
     __syncthreads();
     const int lx = threadIdx.x % TW, ly = threadIdx.x / TW;
     const int x = x0 + lx, y = y0 + ly;
     unsigned int evals = 0;
     if (x < g.W && y < g.H) {
-        const int ce = (ly + g.reach) * t.ww + lx + g.reach;
+        const int ce = (ly + g.reach) * t.wwc + lx + g.reach;
         const size_t i = (size_t)y * g.W + x;
         double d = depth[i];
         double nx = normal[3 * i], ny = normal[3 * i + 1], nz = normal[3 * i + 2];
@@ -499,6 +530,11 @@ static bool make_fast_group(const GroupDev& gd, FastGroup* out) {
     static const double CQ[8] = {-1.223553911532e-03, 6.510368059701e-03, -1.682974898800e-02, 3.068214201158e-02,
                                  -5.008467775423e-02, 8.895977933699e-02, -2.145970563340e-01, 1.570796263346e00};
     for (int i = 0; i < 8; ++i) { g.ca[i] = CA[i]; g.cq[i] = CQ[i]; }
+    if ((unsigned long long)(pitch * rows) * (unsigned long long)gd.V >= (1ull << 32)) return false;
+    g.plane32 = (unsigned)(pitch * rows);
+    g.neg_par_eps = -D360_PARALLEL_EPS;
+    g.tiny = 1e-30;
+    g.c0375 = 0.375;
     g.trunc = gd.trunc;
     g.inv_s = 1.0 / gd.S;
     g.den_lim = nextafterf((float)(-D360_PARALLEL_EPS), -1.0f);
@@ -534,7 +570,7 @@ using namespace fast;
 int fast_eval(const GroupDev& gd, const float* depth, const float* normal, float* cost_out, cudaStream_t s) {
     FastGroup g;
     if (!make_fast_group(gd, &g)) return -1;
-    const size_t smem = tile_bytes(TW, TH_FULL, g.reach, gd.V);
+    const size_t smem = tile_bytes(TW, TH_FULL, g.reach, false, gd.V);
     if (smem > 200 * 1024) return -1;
     dim3 grid((gd.W + TW - 1) / TW, (gd.H + TH_FULL - 1) / TH_FULL);
     D360_FAST_DISPATCH(gd.V, {
@@ -550,7 +586,7 @@ int fast_red_black(const GroupDev& gd, int parity, const float* di, const float*
                    float* nout, float* cout, unsigned long long* n_evals, cudaStream_t s) {
     FastGroup g;
     if (!make_fast_group(gd, &g)) return -1;
-    const size_t smem = tile_bytes(TW, TH_RB, g.reach, gd.V);
+    const size_t smem = tile_bytes(TW, TH_RB, g.reach, (g.stride & 1) == 0, gd.V);
     if (smem > 200 * 1024) return -1;
     dim3 grid((gd.W + TW - 1) / TW, (gd.H + TH_RB - 1) / TH_RB);
     D360_FAST_DISPATCH(gd.V, {
@@ -566,7 +602,7 @@ int fast_refine(const GroupDev& gd, const RefineTable& tab, float* depth, float*
                 unsigned long long* n_evals, cudaStream_t s) {
     FastGroup g;
     if (!make_fast_group(gd, &g)) return -1;
-    const size_t smem = tile_bytes(TW, TH_FULL, g.reach, gd.V);
+    const size_t smem = tile_bytes(TW, TH_FULL, g.reach, false, gd.V);
     if (smem > 200 * 1024) return -1;
     dim3 grid((gd.W + TW - 1) / TW, (gd.H + TH_FULL - 1) / TH_FULL);
     D360_FAST_DISPATCH(gd.V, {
