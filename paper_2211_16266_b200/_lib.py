@@ -18,7 +18,10 @@ MAX_SAMPLES = 128
 MAX_REFINE = 16
 MAX_FRAMES = 8
 
-_LIB_PATH = Path(__file__).resolve().parent / "libd360.so"
+import os
+
+# D360_LIB_PATH selects another build of the same ABI (kernel-variant experiments only)
+_LIB_PATH = Path(os.environ.get("D360_LIB_PATH") or Path(__file__).resolve().parent / "libd360.so")
 _lib = None
 
 c_void = C.c_void_p

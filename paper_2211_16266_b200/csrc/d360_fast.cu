@@ -137,13 +137,21 @@ __device__ __forceinline__ void pixel_stats(const FastGroup& g, const Tile& t, i
 __device__ __forceinline__ double rcp3(double x) {
     const double y = rcp_seed(x);
     const double e = fma(-x, y, 1.0);
+#ifdef D360_NEWTON2
+    return fma(y, e, y);
+#else
     return fma(y, fma(e, e, e), y);
+#endif
 }
 // 1/sqrt(x), third-order refinement of the MUFU.RSQ64H seed
 __device__ __forceinline__ double rsqrt3(double x, double c0375) {
     const double y = rsqrt_seed(x);
     const double e = fma(-(x * y), y, 1.0);
+#ifdef D360_NEWTON2
+    return fma(y * e, 0.5, y);
+#else
     return fma(y * e, fma(e, c0375, 0.5), y);
+#endif
 }
 
 // (u, v) of K:244-258 for one neighbour-frame point t, rounded to f32 like the reference's
@@ -153,9 +161,19 @@ __device__ __forceinline__ void project(const FastGroup& g, double tx, double ty
     // latitude: v = acos_poly(-ty / |t|) * H/pi - 0.5  (K:102-131)
     const double r2 = fma(tz, tz, fma(ty, ty, fma(tx, tx, g.tiny)));
     const double a = fabs(ty) * rsqrt3(r2, g.c0375);
+#ifdef D360_ESTRIN
+    double q;
+    {
+        const double a2 = a * a, a4 = a2 * a2;
+        const double b3 = fma(g.cq[0], a, g.cq[1]), b2 = fma(g.cq[2], a, g.cq[3]);
+        const double b1 = fma(g.cq[4], a, g.cq[5]), b0 = fma(g.cq[6], a, g.cq[7]);
+        q = fma(fma(b3, a2, b2), a4, fma(b1, a2, b0));
+    }
+#else
     double q = g.cq[0];
 #pragma unroll
     for (int i = 1; i < 8; ++i) q = fma(a, q, g.cq[i]);
+#endif
     const double w = 1.0 - a;
     const double sq = w * rsqrt3(w, g.c0375);
     const int hem = (unsigned)__double2hiint(ty) >> 31 ^ 1;  // 1 when ty >= +0: sphi <= -0 (K:131)
@@ -167,9 +185,19 @@ __device__ __forceinline__ void project(const FastGroup& g, double tx, double ty
     const double hi = swap ? tx : tz, lo = swap ? tz : tx;
     const double r = lo * rcp3(hi);  // signed; only |r| is used (abs is a free operand modifier)
     const double s = r * r;
+#ifdef D360_ESTRIN
+    double p;
+    {
+        const double s2 = s * s, s4 = s2 * s2;
+        const double b3 = fma(g.ca[0], s, g.ca[1]), b2 = fma(g.ca[2], s, g.ca[3]);
+        const double b1 = fma(g.ca[4], s, g.ca[5]), b0 = fma(g.ca[6], s, g.ca[7]);
+        p = fma(fma(b3, s2, b2), s4, fma(b1, s2, b0));
+    }
+#else
     double p = g.ca[0];
 #pragma unroll
     for (int i = 1; i < 8; ++i) p = fma(s, p, g.ca[i]);
+#endif
     const int oct = (swap ? 1 : 0) + 2 * (hz >> 31) + 4 * (hx >> 31);
     pu = (float)fma(fabs(r) * p, g.mu[oct], g.cu[oct]);
 }
@@ -234,9 +262,17 @@ __device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, i
         if (ndota >= -D360_FACING_EPS || sr < D360_SIGMA_EPS) return trunc;
         num = __dmul_rn(d, ndota);
     }
+#ifdef D360_ACC32
+    // mean-shifted f32 sums: a = val - mr, b = ref - mr
+    const float mrf = (float)mr;
+    float a0[VT], a1[VT], a2[VT];
+#pragma unroll
+    for (int v = 0; v < VT; ++v) a0[v] = a1[v] = a2[v] = 0.0f;
+#else
     double s0[VT], ss0[VT], rs0[VT];
 #pragma unroll
     for (int v = 0; v < VT; ++v) s0[v] = ss0[v] = rs0[v] = 0.0;
+#endif
     bool bad = false;
 
     const int half = (g.ns - 1) / 2;
@@ -257,7 +293,9 @@ __device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, i
                 dn = par ? g.neg_par_eps : den;
             }
             const double lam = num * rcp3(dn);
+#ifndef D360_ACC32
             const double rv = (double)q.w;
+#endif
             const double* rqe = t.rq + e;
 #pragma unroll
             for (int v = 0; v < VT; ++v) {
@@ -266,10 +304,17 @@ __device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, i
                 const double tz = fma(lam, rqe[(v * 3 + 2) * t.ne], g.rel_t[v][2]);
                 float pu, pv;
                 project(g, tx, ty, tz, pu, pv);
+#ifdef D360_ACC32
+                const float valf = bilinear(g, v * g.plane32, pu, pv) - mrf;
+                a0[v] += valf;
+                a1[v] = fmaf(valf, valf, a1[v]);
+                a2[v] = fmaf(q.w - mrf, valf, a2[v]);
+#else
                 const double val = (double)bilinear(g, v * g.plane32, pu, pv);
                 s0[v] += val;
                 ss0[v] = fma(val, val, ss0[v]);
                 rs0[v] = fma(rv, val, rs0[v]);
+#endif
             }
             e += t.sx;
         }
@@ -282,10 +327,20 @@ __device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, i
 #pragma unroll
     for (int v = 0; v < VT; ++v) {
         cv[v] = trunc;
+#ifdef D360_ACC32
+        // sums of shifted values: mean(b) = mr - mrf (tiny), so cov = E[ab] - E[a] E[b]
+        const double ma = (double)a0[v] * inv_s;
+        const double m0 = ma + (double)mrf;
+        const double v0 = (double)a1[v] * inv_s - ma * ma;
+        (void)m0;
+        if (!(v0 < D360_VAR_EPS)) {
+            const double cov = (double)a2[v] * inv_s - ma * (mr - (double)mrf);
+#else
         const double m0 = s0[v] * inv_s;
         const double v0 = ss0[v] * inv_s - m0 * m0;
         if (!(v0 < D360_VAR_EPS)) {
             const double cov = rs0[v] * inv_s - mr * m0;
+#endif
             double c = 1.0 - cov / (sr * sqrt(v0));
             c = c < 0.0 ? 0.0 : c;
             c = c > trunc ? trunc : c;

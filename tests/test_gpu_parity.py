@@ -408,3 +408,70 @@ def test_full_size_properties(pkg):
     engine.random_init_device(pm3, dr, 0, "philox")
     pm3, pano3 = engine.run_patchmatch_device(prep, pm3, 4, 0)
     assert torch.equal(pm3.depth, pm2.depth) and torch.equal(pm3.cost, pm2.cost)
+
+
+def _oracle_group(oracle, group, hw, stride, top_k=None):
+    return oracle.Group(group.reference.image, [nb.image for nb in group.neighbors],
+                        (group.reference.pose.rotation, group.reference.pose.translation),
+                        [(nb.pose.rotation, nb.pose.translation) for nb in group.neighbors], hw, stride, 1.2,
+                        top_k=top_k)
+
+
+def test_full_size_costs_vs_oracle_c3(pkg, oracle):
+    """BASELINE config C3 geometry (1920x960, V=4, 25 samples): the f32 rounding of u is coarsest
+    here (one ulp = 1.2e-4 px), which is the hardest case for the 1e-4 relative cost parity.
+    Near-ground-truth hypotheses (low costs) on every pixel, throughput kernel vs oracle."""
+    p, engine, _, synth = pkg
+    cam = p.EquirectCamera(1920, 960)
+    group, gt = synth.make_group(synth.default_scene("box"), cam, n_views=4)
+    spec = engine.PatchSpec()
+    prep = engine.prepare_group(group, spec)
+    og = _oracle_group(oracle, group, 5, 2)
+    rng = np.random.default_rng(0)
+    rays = p.camera_rays(cam)
+    n = -rays + rng.normal(0, 0.15, rays.shape)
+    n = (n / np.linalg.norm(n, axis=-1, keepdims=True)).astype(np.float32)
+    d = (gt * (1 + rng.normal(0, 0.01, gt.shape))).astype(np.float32)
+    pm = engine.DevicePlaneMap.from_host(engine.PlaneMap(cam, d, n, np.full(cam.shape, np.inf, np.float32),
+                                                         np.ones(cam.shape, bool), (0.5, 16.0)))
+    engine.evaluate_costs_device(prep, pm)
+    got = pm.cost.cpu().numpy()
+    want = oracle.eval_costs(og, d, n)
+    ok = cost_close(got, want)
+    assert np.median(want) < 0.01  # the regime where a relative tolerance is hard
+    # flips of a rounded (u, v) are possible in principle (f64 noise at an f32 rounding boundary)
+    assert ok.mean() >= 1 - 1e-5, (1 - ok.mean(), np.abs(got - want).max())
+    assert np.abs(got.astype(np.float64) - want).max() <= 2e-6
+
+
+def test_c2_config_passes_vs_oracle(pkg, oracle):
+    """BASELINE config C2 (960x480, V=4, 7x7 patch = 49 samples at stride 1): odd stride, so the
+    red-black tile is not colour-compressed.  One red-black pass and one refinement vs oracle."""
+    p, engine, _, synth = pkg
+    cam = p.EquirectCamera(960, 480)
+    group, gt = synth.make_group(synth.default_scene("box"), cam, n_views=4)
+    spec = engine.PatchSpec(3, 1, 1.2)
+    prep = engine.prepare_group(group, spec)
+    og = _oracle_group(oracle, group, 3, 1)
+    dr = (0.5, 16.0)
+    init = engine.random_init(engine.PlaneMap.empty(cam, dr), dr, seed=11)
+    rays = p.camera_rays(cam)
+    init.depth[:, ::3] = gt[:, ::3]
+    init.normal[:, ::3] = (-rays[:, ::3]).astype(np.float32)
+    src = engine.DevicePlaneMap.from_host(init)
+    engine.evaluate_costs_device(prep, src)
+    c0 = src.cost.cpu().numpy()
+    assert cost_close(c0, oracle.eval_costs(og, init.depth, init.normal)).all()
+    dst = src.clone()
+    engine.red_black_pass_device(prep, 0, src, dst)
+    od, on, oc, _ = oracle.red_black_pass(og, 0, init.depth, init.normal, c0)
+    gd, gc = dst.depth.cpu().numpy(), dst.cost.cpu().numpy()
+    same = gd == od
+    assert same.mean() >= 1 - 1e-4 and cost_close(gc[same], oc[same]).all()
+    tabs = oracle.refinement_draw_tables(5, 1, dr)
+    engine.refine_pass_device(prep, dst, tabs[0], dr)
+    rd, rn, rc = oracle.refine_pass(og, gd, dst.normal.cpu().numpy() if False else on, gc if False else oc, tabs[0], dr)
+    got_d, got_c = dst.depth.cpu().numpy(), dst.cost.cpu().numpy()
+    same2 = same & (got_d == rd)
+    assert same2.mean() >= 1 - 2e-4
+    assert cost_close(got_c[same2], rc[same2]).all()
