@@ -34,6 +34,7 @@ class Group(C.Structure):
         ("width", C.c_int32), ("height", C.c_int32), ("n_views", C.c_int32), ("n_samples", C.c_int32),
         ("top_k", C.c_int32), ("precision", C.c_int32),
         ("rays", c_void), ("ref_gray", c_void), ("nb", c_void), ("nb_pad_x", C.c_int32), ("nb_pad_y", C.c_int32),
+        ("nb64", c_void),
         ("rel_r", c_void), ("rel_t", c_void), ("offsets", c_void),
         ("trunc", C.c_double),
     ]
@@ -52,7 +53,7 @@ _SIGNATURES = {
                                                                          C.c_double, c_void, c_void, c_void]),
     "d360_median_support_mask": (C.c_int, [c_void, c_void, C.c_int, C.c_double, c_void, C.c_int, C.c_int, c_void]),
     "d360_to_gray": (C.c_int, [c_void, C.c_int, c_void, C.c_int, C.c_int, c_void]),
-    "d360_to_gray_padded": (C.c_int, [c_void, C.c_int, c_void, C.c_int, C.c_int, C.c_int, C.c_int, c_void]),
+    "d360_to_gray_padded": (C.c_int, [c_void, C.c_int, c_void, c_void, C.c_int, C.c_int, C.c_int, C.c_int, c_void]),
     "d360_camera_rays": (C.c_int, [c_void] * 6 + [C.c_int, C.c_int, c_void]),
     "d360_random_init": (C.c_int, [c_void] * 6 + [C.c_uint64, C.c_double, C.c_double, c_void, C.c_int, C.c_int,
                                                   c_void]),

@@ -24,14 +24,16 @@ __device__ __forceinline__ float luma_of(const uint8_t* __restrict__ img, int ch
 }
 
 // Output raster (H + 2 pad_y, W + 2 pad_x): columns wrap, rows replicate (pads may be 0).
-__global__ void k_to_gray(const uint8_t* __restrict__ img, int channels, float* __restrict__ gray, int H, int W,
-                          int pad_x, int pad_y) {
+__global__ void k_to_gray(const uint8_t* __restrict__ img, int channels, float* __restrict__ gray,
+                          double* __restrict__ gray64, int H, int W, int pad_x, int pad_y) {
     const int pw = W + 2 * pad_x, ph = H + 2 * pad_y;
     const int px = blockIdx.x * blockDim.x + threadIdx.x, py = blockIdx.y;
     if (px >= pw || py >= ph) return;
     const int x = pos_mod(px - pad_x, W);
     const int y = min(max(py - pad_y, 0), H - 1);
-    gray[(size_t)py * pw + px] = luma_of(img, channels, (size_t)y * W + x);
+    const float l = luma_of(img, channels, (size_t)y * W + x);
+    if (gray != nullptr) gray[(size_t)py * pw + px] = l;
+    if (gray64 != nullptr) gray64[(size_t)py * pw + px] = (double)l;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -548,8 +550,8 @@ static int fill_frames(Frames* f, const float* const* depth, const uint8_t* cons
 
 using namespace d360;
 
-extern "C" int d360_to_gray_padded(const uint8_t* image, int channels, float* gray, int height, int width,
-                                   int pad_x, int pad_y, void* stream) {
+extern "C" int d360_to_gray_padded(const uint8_t* image, int channels, float* gray, double* gray64, int height,
+                                   int width, int pad_x, int pad_y, void* stream) {
     if (channels != 1 && channels != 3) {
         set_error("expected (H, W) or (H, W, 3) image, got %d channels", channels);
         return 1;
@@ -561,14 +563,15 @@ extern "C" int d360_to_gray_padded(const uint8_t* image, int channels, float* gr
     dim3 grid((width + 2 * pad_x + 255) / 256, height + 2 * pad_y);
     {
         TraceScope ts_("to_gray", (cudaStream_t)stream);
-        k_to_gray<<<grid, 256, 0, (cudaStream_t)stream>>>(image, channels, gray, height, width, pad_x, pad_y);
+        k_to_gray<<<grid, 256, 0, (cudaStream_t)stream>>>(image, channels, gray, gray64, height, width, pad_x,
+                                                          pad_y);
     }
     return check_launch("to_gray");
 }
 
 extern "C" int d360_to_gray(const uint8_t* image, int channels, float* gray, int height, int width,
                             void* stream) {
-    return d360_to_gray_padded(image, channels, gray, height, width, 0, 0, stream);
+    return d360_to_gray_padded(image, channels, gray, nullptr, height, width, 0, 0, stream);
 }
 
 extern "C" int d360_camera_rays(const double* sin_lam, const double* cos_lam, const double* sin_phi,

@@ -107,6 +107,7 @@ int make_group_dev(const d360_group* g, GroupDev* out) {
         return 1;
     }
     d.nb_pad_x = g->nb_pad_x; d.nb_pad_y = g->nb_pad_y;
+    d.nb64 = g->nb64;
     int reach = 0;
     for (int k = 0; k < g->n_samples; ++k) {
         const int dx = g->offsets[2 * k], dy = g->offsets[2 * k + 1];

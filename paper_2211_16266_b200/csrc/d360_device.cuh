@@ -26,6 +26,7 @@ struct GroupDev {
     const float* rays;
     const float* ref_gray;
     const float* nb;
+    const double* nb64;  // optional f64 copy of the padded neighbour planes (d360.h)
     float rel_r[D360_MAX_VIEWS][9];
     float rel_t[D360_MAX_VIEWS][3];
     signed char dx[D360_MAX_SAMPLES];

@@ -38,7 +38,7 @@ struct FastGroup {
     size_t plane;         // elements per neighbour plane
     const float* rays;
     const float* ref_gray;
-    const float* nb;      // padded planes, see d360.h
+    const double* nb64;   // padded planes widened to f64, see d360.h
     float rel_r[D360_MAX_VIEWS][9];
     double rel_t[D360_MAX_VIEWS][3];
     double mu[8], cu[8];  // longitude: u = p * mu[oct] + cu[oct]
@@ -202,29 +202,31 @@ __device__ __forceinline__ void project(const FastGroup& g, double tx, double ty
     pu = (float)fma(fabs(r) * p, g.mu[oct], g.cu[oct]);
 }
 
-// K:134-153 on the f32 (u, v); weights and lerps in f32 (policy MIXED).  The plane is padded
+// K:134-153 on the f32 (u, v), interpolated in f64 like the reference (the planes are stored
+// widened, so the taps need no conversion; an f32 lerp costs up to 1e-2 relative on the cost of
+// low-texture patches, measured).  The plane is padded
 // (wrapped columns, replicated rows), so floor(u), floor(u)+1, floor(v), floor(v)+1 are all
 // in-plane and the reference's wrap / clamp rules are data, not code.  floor by the
 // 1.5 * 2^23 magic add; the element index is formed in f32 (exact below 2^23) and read out of
 // the mantissa, so no F2I / I2F conversions are issued.
-__device__ __forceinline__ float bilinear(const FastGroup& g, unsigned view_off, float u, float v) {
+__device__ __forceinline__ double bilinear(const FastGroup& g, unsigned view_off, float u, float v) {
     const float MAGIC = 12582912.0f;
     float fl_u = __fadd_rn(__fadd_rn(u, MAGIC), -MAGIC);
     if (fl_u > u) fl_u -= 1.0f;
     float fl_v = __fadd_rn(__fadd_rn(v, MAGIC), -MAGIC);
     if (fl_v > v) fl_v -= 1.0f;
-    const float fu = u - fl_u, fv = v - fl_v;
+    const double fu = (double)(u - fl_u), fv = (double)(v - fl_v);  // the f32 differences are exact
     const float off = __fadd_rn(fmaf(fl_v, g.pitch_f, fl_u), g.idx_bias);
     // min: only non-finite (u, v) can exceed it.  All offsets are 32-bit element indices from
     // one 64-bit base, so each tap costs one IMAD.WIDE.
     const unsigned idx = min((unsigned)__float_as_int(off) & 0x7fffffu, g.max_idx) + view_off;
-    const float* __restrict__ nb = g.nb;
-    const float a = __ldg(nb + idx), b = __ldg(nb + idx + 1u);
+    const double* __restrict__ nb = g.nb64;
+    const double a = __ldg(nb + idx), b = __ldg(nb + idx + 1u);
     const unsigned idx1 = idx + (unsigned)g.pitch;
-    const float c = __ldg(nb + idx1), d = __ldg(nb + idx1 + 1u);
-    const float top = fmaf(b - a, fu, a);
-    const float bot = fmaf(d - c, fu, c);
-    return fmaf(bot - top, fv, top);
+    const double c = __ldg(nb + idx1), d = __ldg(nb + idx1 + 1u);
+    const double top = fma(b - a, fu, a);
+    const double bot = fma(d - c, fu, c);
+    return fma(bot - top, fv, top);
 }
 
 template <int VT>
@@ -310,7 +312,7 @@ __device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, i
                 a1[v] = fmaf(valf, valf, a1[v]);
                 a2[v] = fmaf(q.w - mrf, valf, a2[v]);
 #else
-                const double val = (double)bilinear(g, v * g.plane32, pu, pv);
+                const double val = bilinear(g, v * g.plane32, pu, pv);
                 s0[v] += val;
                 ss0[v] = fma(val, val, ss0[v]);
                 rs0[v] = fma(rv, val, rs0[v]);
@@ -553,7 +555,7 @@ static bool make_fast_group(const GroupDev& gd, FastGroup* out) {
     for (int k = 0; k < gd.S; ++k) {
         if (gd.dx[k] != (k % ns - half) * stride || gd.dy[k] != (k / ns - half) * stride) return false;
     }
-    if (gd.nb_pad_x < 1 || gd.nb_pad_y < 1) return false;  // needs the padded neighbour planes
+    if (gd.nb_pad_x < 1 || gd.nb_pad_y < 1 || gd.nb64 == nullptr) return false;  // needs padded f64 planes
     const long long pitch = gd.W + 2 * gd.nb_pad_x, rows = gd.H + 2 * gd.nb_pad_y;
     if (pitch * rows >= (1ll << 23)) return false;  // f32 index arithmetic must stay exact
     FastGroup& g = *out;
@@ -563,7 +565,7 @@ static bool make_fast_group(const GroupDev& gd, FastGroup* out) {
     g.max_idx = (unsigned)(pitch * rows - pitch - 2);
     g.pitch_f = (float)pitch;
     g.idx_bias = 8388608.0f + (float)(gd.nb_pad_y * pitch + gd.nb_pad_x);
-    g.rays = gd.rays; g.ref_gray = gd.ref_gray; g.nb = gd.nb;
+    g.rays = gd.rays; g.ref_gray = gd.ref_gray; g.nb64 = gd.nb64;
     for (int v = 0; v < gd.V; ++v) {
         for (int i = 0; i < 9; ++i) g.rel_r[v][i] = gd.rel_r[v][i];
         for (int i = 0; i < 3; ++i) g.rel_t[v][i] = (double)gd.rel_t[v][i];

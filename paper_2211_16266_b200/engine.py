@@ -224,13 +224,15 @@ NB_PAD_X = 4  # wrapped columns each side of a neighbour plane (keeps rows 16-by
 NB_PAD_Y = 1  # replicated rows above / below
 
 
-def to_gray_device(image, device=None, out: torch.Tensor | None = None, pad=(0, 0)) -> torch.Tensor:
+def to_gray_device(image, device=None, out: torch.Tensor | None = None, pad=(0, 0),
+                   out64: torch.Tensor | None = None) -> torch.Tensor:
     """uint8 (H,W) / (H,W,3) numpy array or CUDA tensor -> float32 luma on the device
     (keyframes.py:64-72, float32 arithmetic).
 
     ``pad=(px, py)`` writes the padded plane layout of ``d360_group.nb``: shape
     (H + 2 py, W + 2 px) with wrapped columns and replicated rows.  ``out``: optional
-    contiguous float32 target of that shape."""
+    contiguous float32 target of that shape; ``out64``: optional float64 target of the same
+    shape that receives the exactly widened values."""
     dev = _device(device)
     lib = _lib.load()
     img = image if isinstance(image, torch.Tensor) else _up(np.asarray(image), np.uint8, dev)
@@ -250,7 +252,10 @@ def to_gray_device(image, device=None, out: torch.Tensor | None = None, pad=(0, 
         out = torch.empty(shape, dtype=torch.float32, device=dev)
     elif tuple(out.shape) != shape or out.dtype != torch.float32 or not out.is_contiguous():
         raise ValueError(f"out must be a contiguous float32 {shape} tensor")
-    _lib.check(lib.d360_to_gray_padded(_ptr(img), ch, _ptr(out), h, w, px, py, _stream()), "to_gray")
+    if out64 is not None and (tuple(out64.shape) != shape or out64.dtype != torch.float64 or
+                              not out64.is_contiguous()):
+        raise ValueError(f"out64 must be a contiguous float64 {shape} tensor")
+    _lib.check(lib.d360_to_gray_padded(_ptr(img), ch, _ptr(out), _ptr(out64), h, w, px, py, _stream()), "to_gray")
     return out
 
 
@@ -289,15 +294,18 @@ class PreparedGroup:
             # neighbour luma planes, padded so that every bilinear footprint is in-plane (d360.h)
             self.nb_padded = torch.empty((self.n_views, h + 2 * NB_PAD_Y, w + 2 * NB_PAD_X), dtype=torch.float32,
                                          device=self.device)
+            # the same planes widened to f64: the reference interpolates in f64 (K:134-153)
+            self.nb64_padded = torch.empty(self.nb_padded.shape, dtype=torch.float64, device=self.device)
             for v, im in enumerate(imgs[1:]):
-                to_gray_device(im, self.device, out=self.nb_padded[v], pad=(NB_PAD_X, NB_PAD_Y))
+                to_gray_device(im, self.device, out=self.nb_padded[v], pad=(NB_PAD_X, NB_PAD_Y),
+                               out64=self.nb64_padded[v])
         rel = [relative_transform(group.reference.pose, nb.pose) for nb in group.neighbors]
         self.rel_r = np.ascontiguousarray(np.stack([r for r, _ in rel]), dtype=np.float32)
         self.rel_t = np.ascontiguousarray(np.stack([t for _, t in rel]), dtype=np.float32)
         self._struct = _lib.Group(
             width=self.camera.width, height=self.camera.height, n_views=self.n_views,
             n_samples=len(self.offsets), top_k=self.top_k, precision=PRECISIONS[self.precision],
-            rays=_ptr(self.cam_dev.rays32), ref_gray=_ptr(self.ref_gray), nb=_ptr(self.nb_padded), nb_pad_x=NB_PAD_X, nb_pad_y=NB_PAD_Y,
+            rays=_ptr(self.cam_dev.rays32), ref_gray=_ptr(self.ref_gray), nb=_ptr(self.nb_padded), nb_pad_x=NB_PAD_X, nb_pad_y=NB_PAD_Y, nb64=_ptr(self.nb64_padded),
             rel_r=self.rel_r.ctypes.data, rel_t=self.rel_t.ctypes.data, offsets=self.offsets.ctypes.data,
             trunc=float(spec.cost_truncation))
 
