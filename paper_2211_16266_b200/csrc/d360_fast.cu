@@ -137,96 +137,114 @@ __device__ __forceinline__ void pixel_stats(const FastGroup& g, const Tile& t, i
 __device__ __forceinline__ double rcp3(double x) {
     const double y = rcp_seed(x);
     const double e = fma(-x, y, 1.0);
-#ifdef D360_NEWTON2
-    return fma(y, e, y);
-#else
     return fma(y, fma(e, e, e), y);
-#endif
 }
 // 1/sqrt(x), third-order refinement of the MUFU.RSQ64H seed
 __device__ __forceinline__ double rsqrt3(double x, double c0375) {
     const double y = rsqrt_seed(x);
     const double e = fma(-(x * y), y, 1.0);
-#ifdef D360_NEWTON2
-    return fma(y * e, 0.5, y);
-#else
     return fma(y * e, fma(e, c0375, 0.5), y);
-#endif
 }
 
-// (u, v) of K:244-258 for one neighbour-frame point t, rounded to f32 like the reference's
-// scratch.  No guards on the two measure-zero singularities (t on the neighbour's polar axis:
-// max(|tx|,|tz|) = 0 or 1 - |ty|/|t| <= 0); they yield NaN, which cand_cost maps to `trunc`.
-__device__ __forceinline__ void project(const FastGroup& g, double tx, double ty, double tz, float& pu, float& pv) {
-    // latitude: v = acos_poly(-ty / |t|) * H/pi - 0.5  (K:102-131)
-    const double r2 = fma(tz, tz, fma(ty, ty, fma(tx, tx, g.tiny)));
-    const double a = fabs(ty) * rsqrt3(r2, g.c0375);
-#ifdef D360_ESTRIN
-    double q;
-    {
-        const double a2 = a * a, a4 = a2 * a2;
-        const double b3 = fma(g.cq[0], a, g.cq[1]), b2 = fma(g.cq[2], a, g.cq[3]);
-        const double b1 = fma(g.cq[4], a, g.cq[5]), b0 = fma(g.cq[6], a, g.cq[7]);
-        q = fma(fma(b3, a2, b2), a4, fma(b1, a2, b0));
-    }
-#else
-    double q = g.cq[0];
+// (u, v) of K:244-258 for the VT neighbour-frame points of one sample, rounded to f32 like the
+// reference's scratch, then the f64 bilinear taps of K:134-153.  Written stage by stage over
+// the views so that the VT independent dependency chains sit next to each other in program
+// order (measured: -8 % on refine_pass versus one view after the other).
+//
+// No guards on the two measure-zero singularities (t on the neighbour's polar axis:
+// max(|tx|,|tz|) = 0, or 1 - |ty|/|t| <= 0); they yield NaN, which cand_cost maps to `trunc`.
+//
+// Bilinear: the planes are padded (wrapped columns, replicated rows), so floor(u), floor(u)+1,
+// floor(v), floor(v)+1 are all in-plane and the reference's wrap / clamp rules are data, not
+// code; they are stored widened to f64 so the taps need no conversion (an f32 lerp costs up to
+// 1e-2 relative on the cost of low-texture patches, measured).  floor by the 1.5 * 2^23 magic
+// add; the element index is formed in f32 (exact below 2^23) and read out of the mantissa, so
+// no F2I / I2F conversions are issued; all offsets are 32-bit element indices from one base.
+#define D360_FORV for (int v = 0; v < VT; ++v)
+template <int VT>
+__device__ __forceinline__ void project_bilinear_all(const FastGroup& g, const double (&tx)[VT], const double (&ty)[VT],
+                                                     const double (&tz)[VT], double (&val)[VT]) {
+    double r2[VT], y1[VT], e1[VT], a[VT], q[VT], w[VT], y2[VT], e2[VT], sq[VT];
 #pragma unroll
-    for (int i = 1; i < 8; ++i) q = fma(a, q, g.cq[i]);
-#endif
-    const double w = 1.0 - a;
-    const double sq = w * rsqrt3(w, g.c0375);
-    const int hem = (unsigned)__double2hiint(ty) >> 31 ^ 1;  // 1 when ty >= +0: sphi <= -0 (K:131)
-    pv = (float)fma(q * sq, g.mv[hem], g.cv[hem]);
-
-    // longitude: u = (atan2_poly(tx, tz) + pi) * W/2pi - 0.5  (K:59-99)
-    const unsigned hx = (unsigned)__double2hiint(tx), hz = (unsigned)__double2hiint(tz);
-    const bool swap = fabs(tx) > fabs(tz);
-    const double hi = swap ? tx : tz, lo = swap ? tz : tx;
-    const double r = lo * rcp3(hi);  // signed; only |r| is used (abs is a free operand modifier)
-    const double s = r * r;
-#ifdef D360_ESTRIN
-    double p;
-    {
-        const double s2 = s * s, s4 = s2 * s2;
-        const double b3 = fma(g.ca[0], s, g.ca[1]), b2 = fma(g.ca[2], s, g.ca[3]);
-        const double b1 = fma(g.ca[4], s, g.ca[5]), b0 = fma(g.ca[6], s, g.ca[7]);
-        p = fma(fma(b3, s2, b2), s4, fma(b1, s2, b0));
-    }
-#else
-    double p = g.ca[0];
+    D360_FORV r2[v] = fma(tz[v], tz[v], fma(ty[v], ty[v], fma(tx[v], tx[v], g.tiny)));
 #pragma unroll
-    for (int i = 1; i < 8; ++i) p = fma(s, p, g.ca[i]);
-#endif
-    const int oct = (swap ? 1 : 0) + 2 * (hz >> 31) + 4 * (hx >> 31);
-    pu = (float)fma(fabs(r) * p, g.mu[oct], g.cu[oct]);
-}
-
-// K:134-153 on the f32 (u, v), interpolated in f64 like the reference (the planes are stored
-// widened, so the taps need no conversion; an f32 lerp costs up to 1e-2 relative on the cost of
-// low-texture patches, measured).  The plane is padded
-// (wrapped columns, replicated rows), so floor(u), floor(u)+1, floor(v), floor(v)+1 are all
-// in-plane and the reference's wrap / clamp rules are data, not code.  floor by the
-// 1.5 * 2^23 magic add; the element index is formed in f32 (exact below 2^23) and read out of
-// the mantissa, so no F2I / I2F conversions are issued.
-__device__ __forceinline__ double bilinear(const FastGroup& g, unsigned view_off, float u, float v) {
+    D360_FORV y1[v] = rsqrt_seed(r2[v]);
+    double hi[VT], lo[VT], y3[VT];
+    bool swap[VT];
+#pragma unroll
+    D360_FORV {
+        swap[v] = fabs(tx[v]) > fabs(tz[v]);
+        hi[v] = swap[v] ? tx[v] : tz[v];
+        lo[v] = swap[v] ? tz[v] : tx[v];
+    }
+#pragma unroll
+    D360_FORV y3[v] = rcp_seed(hi[v]);
+#pragma unroll
+    D360_FORV e1[v] = fma(-(r2[v] * y1[v]), y1[v], 1.0);
+    double e3[VT];
+#pragma unroll
+    D360_FORV e3[v] = fma(-hi[v], y3[v], 1.0);
+#pragma unroll
+    D360_FORV y1[v] = fma(y1[v] * e1[v], fma(e1[v], g.c0375, 0.5), y1[v]);
+#pragma unroll
+    D360_FORV y3[v] = fma(y3[v], fma(e3[v], e3[v], e3[v]), y3[v]);
+#pragma unroll
+    D360_FORV a[v] = fabs(ty[v]) * y1[v];
+    double r[VT], s[VT], p[VT];
+#pragma unroll
+    D360_FORV { r[v] = lo[v] * y3[v]; s[v] = r[v] * r[v]; }
+#pragma unroll
+    D360_FORV { w[v] = 1.0 - a[v]; y2[v] = rsqrt_seed(w[v]); }
+#pragma unroll
+    D360_FORV { q[v] = g.cq[0]; p[v] = g.ca[0]; }
+#pragma unroll
+    for (int i = 1; i < 8; ++i) {
+#pragma unroll
+        D360_FORV { q[v] = fma(a[v], q[v], g.cq[i]); p[v] = fma(s[v], p[v], g.ca[i]); }
+    }
+#pragma unroll
+    D360_FORV e2[v] = fma(-(w[v] * y2[v]), y2[v], 1.0);  // (the compiler shares w y2 with s0 below)
+#pragma unroll
+    D360_FORV {  // sqrt(w) = s0 (1 + e/2 + 3e^2/8), s0 = w y2
+        const double s0 = w[v] * y2[v];
+        sq[v] = fma(s0 * e2[v], fma(e2[v], g.c0375, 0.5), s0);
+    }
+    float pu[VT], pv[VT];
+#pragma unroll
+    D360_FORV {
+        const int hem = (unsigned)__double2hiint(ty[v]) >> 31 ^ 1;
+        pv[v] = (float)fma(q[v] * sq[v], g.mv[hem], g.cv[hem]);
+        const unsigned hx = (unsigned)__double2hiint(tx[v]), hz = (unsigned)__double2hiint(tz[v]);
+        const int oct = (swap[v] ? 1 : 0) + 2 * (hz >> 31) + 4 * (hx >> 31);
+        pu[v] = (float)fma(fabs(r[v]) * p[v], g.mu[oct], g.cu[oct]);
+    }
     const float MAGIC = 12582912.0f;
-    float fl_u = __fadd_rn(__fadd_rn(u, MAGIC), -MAGIC);
-    if (fl_u > u) fl_u -= 1.0f;
-    float fl_v = __fadd_rn(__fadd_rn(v, MAGIC), -MAGIC);
-    if (fl_v > v) fl_v -= 1.0f;
-    const double fu = (double)(u - fl_u), fv = (double)(v - fl_v);  // the f32 differences are exact
-    const float off = __fadd_rn(fmaf(fl_v, g.pitch_f, fl_u), g.idx_bias);
-    // min: only non-finite (u, v) can exceed it.  All offsets are 32-bit element indices from
-    // one 64-bit base, so each tap costs one IMAD.WIDE.
-    const unsigned idx = min((unsigned)__float_as_int(off) & 0x7fffffu, g.max_idx) + view_off;
+    float fl_u[VT], fl_v[VT];
+#pragma unroll
+    D360_FORV { fl_u[v] = __fadd_rn(__fadd_rn(pu[v], MAGIC), -MAGIC); fl_v[v] = __fadd_rn(__fadd_rn(pv[v], MAGIC), -MAGIC); }
+#pragma unroll
+    D360_FORV { if (fl_u[v] > pu[v]) fl_u[v] -= 1.0f; if (fl_v[v] > pv[v]) fl_v[v] -= 1.0f; }
+    unsigned idx[VT];
+#pragma unroll
+    D360_FORV {
+        const float off = __fadd_rn(fmaf(fl_v[v], g.pitch_f, fl_u[v]), g.idx_bias);
+        idx[v] = min((unsigned)__float_as_int(off) & 0x7fffffu, g.max_idx) + v * g.plane32;
+    }
     const double* __restrict__ nb = g.nb64;
-    const double a = __ldg(nb + idx), b = __ldg(nb + idx + 1u);
-    const unsigned idx1 = idx + (unsigned)g.pitch;
-    const double c = __ldg(nb + idx1), d = __ldg(nb + idx1 + 1u);
-    const double top = fma(b - a, fu, a);
-    const double bot = fma(d - c, fu, c);
-    return fma(bot - top, fv, top);
+    double ta[VT], tb[VT], tc[VT], td[VT];
+#pragma unroll
+    D360_FORV {
+        ta[v] = __ldg(nb + idx[v]); tb[v] = __ldg(nb + idx[v] + 1u);
+        const unsigned idx1 = idx[v] + (unsigned)g.pitch;
+        tc[v] = __ldg(nb + idx1); td[v] = __ldg(nb + idx1 + 1u);
+    }
+#pragma unroll
+    D360_FORV {
+        const double fu = (double)(pu[v] - fl_u[v]), fv = (double)(pv[v] - fl_v[v]);
+        const double top = fma(tb[v] - ta[v], fu, ta[v]);
+        const double bot = fma(td[v] - tc[v], fu, tc[v]);
+        val[v] = fma(bot - top, fv, top);
+    }
 }
 
 template <int VT>
@@ -264,17 +282,9 @@ __device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, i
         if (ndota >= -D360_FACING_EPS || sr < D360_SIGMA_EPS) return trunc;
         num = __dmul_rn(d, ndota);
     }
-#ifdef D360_ACC32
-    // mean-shifted f32 sums: a = val - mr, b = ref - mr
-    const float mrf = (float)mr;
-    float a0[VT], a1[VT], a2[VT];
-#pragma unroll
-    for (int v = 0; v < VT; ++v) a0[v] = a1[v] = a2[v] = 0.0f;
-#else
     double s0[VT], ss0[VT], rs0[VT];
 #pragma unroll
     for (int v = 0; v < VT; ++v) s0[v] = ss0[v] = rs0[v] = 0.0;
-#endif
     bool bad = false;
 
     const int half = (g.ns - 1) / 2;
@@ -295,28 +305,23 @@ __device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, i
                 dn = par ? g.neg_par_eps : den;
             }
             const double lam = num * rcp3(dn);
-#ifndef D360_ACC32
             const double rv = (double)q.w;
-#endif
             const double* rqe = t.rq + e;
+            {
+                double tx[VT], ty[VT], tz[VT], val[VT];
 #pragma unroll
-            for (int v = 0; v < VT; ++v) {
-                const double tx = fma(lam, rqe[(v * 3 + 0) * t.ne], g.rel_t[v][0]);
-                const double ty = fma(lam, rqe[(v * 3 + 1) * t.ne], g.rel_t[v][1]);
-                const double tz = fma(lam, rqe[(v * 3 + 2) * t.ne], g.rel_t[v][2]);
-                float pu, pv;
-                project(g, tx, ty, tz, pu, pv);
-#ifdef D360_ACC32
-                const float valf = bilinear(g, v * g.plane32, pu, pv) - mrf;
-                a0[v] += valf;
-                a1[v] = fmaf(valf, valf, a1[v]);
-                a2[v] = fmaf(q.w - mrf, valf, a2[v]);
-#else
-                const double val = bilinear(g, v * g.plane32, pu, pv);
-                s0[v] += val;
-                ss0[v] = fma(val, val, ss0[v]);
-                rs0[v] = fma(rv, val, rs0[v]);
-#endif
+                for (int v = 0; v < VT; ++v) {
+                    tx[v] = fma(lam, rqe[(v * 3 + 0) * t.ne], g.rel_t[v][0]);
+                    ty[v] = fma(lam, rqe[(v * 3 + 1) * t.ne], g.rel_t[v][1]);
+                    tz[v] = fma(lam, rqe[(v * 3 + 2) * t.ne], g.rel_t[v][2]);
+                }
+                project_bilinear_all<VT>(g, tx, ty, tz, val);
+#pragma unroll
+                for (int v = 0; v < VT; ++v) {
+                    s0[v] += val[v];
+                    ss0[v] = fma(val[v], val[v], ss0[v]);
+                    rs0[v] = fma(rv, val[v], rs0[v]);
+                }
             }
             e += t.sx;
         }
@@ -329,20 +334,10 @@ __device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, i
 #pragma unroll
     for (int v = 0; v < VT; ++v) {
         cv[v] = trunc;
-#ifdef D360_ACC32
-        // sums of shifted values: mean(b) = mr - mrf (tiny), so cov = E[ab] - E[a] E[b]
-        const double ma = (double)a0[v] * inv_s;
-        const double m0 = ma + (double)mrf;
-        const double v0 = (double)a1[v] * inv_s - ma * ma;
-        (void)m0;
-        if (!(v0 < D360_VAR_EPS)) {
-            const double cov = (double)a2[v] * inv_s - ma * (mr - (double)mrf);
-#else
         const double m0 = s0[v] * inv_s;
         const double v0 = ss0[v] * inv_s - m0 * m0;
         if (!(v0 < D360_VAR_EPS)) {
             const double cov = rs0[v] * inv_s - mr * m0;
-#endif
             double c = 1.0 - cov / (sr * sqrt(v0));
             c = c < 0.0 ? 0.0 : c;
             c = c > trunc ? trunc : c;
@@ -376,10 +371,27 @@ __global__ void __launch_bounds__(THREADS, D360_FAST_MINB)
 }
 
 // ---------------------------------------------------------------------------------------
-// red_black_pass, K:352-473.  A CTA covers TW x TH_RB pixels; each of its 256 threads owns one
-// pixel of the requested colour and carries its off-colour neighbour over unchanged.
+// red_black_pass, K:352-473.  A CTA covers TW x TH_RB pixels, 256 of them of the requested
+// colour.  The number of candidates a pixel has to evaluate varies (0..8 after the duplicate
+// skipping of K:418-432), so the work is levelled through a CTA-wide queue:
+//   phase 1  one thread per pixel: in-range, non-duplicate neighbours -> candidate mask;
+//            patch statistics; exclusive scan of the counts; (pixel, neighbour) items queued;
+//   phase 2  warps pull 32 items at a time and evaluate them (any lane, any pixel of the tile);
+//   phase 3  one thread per pixel: strict-< arg-min over its candidates in neighbour order
+//            (K:463; the cost of a hypothesis does not depend on evaluation order, so this is
+//            the reference's sequential accept).
 // ---------------------------------------------------------------------------------------
 __constant__ int c_nbr2[8][2] = {{-1, -1}, {1, -1}, {-1, 1}, {1, 1}, {0, -2}, {0, 2}, {-2, 0}, {2, 0}};
+
+struct RbQueue {
+    double2 stats[THREADS];            // (mr, sr) per pixel
+    double costs[THREADS * 8];         // cost of neighbour j's hypothesis at pixel p
+    unsigned short items[THREADS * 8]; // p * 8 + j
+    int warp_totals[THREADS / 32];
+    int total, next;
+};
+
+__host__ __device__ inline size_t rb_queue_offset(size_t tile) { return (tile + 15) & ~(size_t)15; }
 
 template <int VT>
 __global__ void __launch_bounds__(THREADS, D360_FAST_MINB)
@@ -389,13 +401,18 @@ __global__ void __launch_bounds__(THREADS, D360_FAST_MINB)
     extern __shared__ __align__(16) unsigned char smem[];
     const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH_RB;  // x0 is even
     const bool compress = (g.stride & 1) == 0;
+    RbQueue& q = *reinterpret_cast<RbQueue*>(smem + rb_queue_offset(tile_bytes(TW, TH_RB, g.reach, compress, VT)));
+    if (threadIdx.x == 0) q.next = 0;
     const Tile t = tile_setup<VT>(g, smem, x0, y0, TH_RB, compress, (parity + y0) & 1);
     __syncthreads();
-    const int ly = threadIdx.x / (TW / 2);
+
+    // ---- phase 1
+    const int tid = threadIdx.x;
+    const int ly = tid / (TW / 2);
     const int y = y0 + ly;
-    const int lx = 2 * (threadIdx.x % (TW / 2)) + ((parity + y) & 1);
+    const int lx = 2 * (tid % (TW / 2)) + ((parity + y) & 1);
     const int x = x0 + lx;
-    unsigned int evals = 0;
+    const bool live = x < g.W && y < g.H;
     if (y < g.H) {
         // carry the off-colour pixel of this pair over unchanged (E:575-577)
         const int xo = x0 + (lx ^ 1);
@@ -408,31 +425,23 @@ __global__ void __launch_bounds__(THREADS, D360_FAST_MINB)
             cost_out[o] = cost_in[o];
         }
     }
-    if (x < g.W && y < g.H) {
-        const size_t i = (size_t)y * g.W + x;
-        // original hypothesis of the pixel: a neighbour equal to it is a duplicate for the whole
-        // pass (its cost is cost_in, which can never beat the running best under strict <)
+    const size_t i = live ? (size_t)y * g.W + x : 0;
+    unsigned mask = 0;
+    if (live) {
+        // K:418-432 skips exact duplicates of the best-so-far and of already evaluated
+        // candidates.  Every earlier in-range neighbour was either evaluated or itself such a
+        // duplicate, so comparing with the pixel's original hypothesis and with the earlier
+        // neighbours selects the same set, except that it also skips re-evaluating the original
+        // hypothesis once it has been displaced, which strict < would reject anyway.
         const float od = depth_in[i];
         const float onx = normal_in[3 * i], ony = normal_in[3 * i + 1], onz = normal_in[3 * i + 2];
-        float bd = od, bnx = onx, bny = ony, bnz = onz;
-        double bc = (double)cost_in[i];
-        const int ce = (ly + g.reach) * t.wwc + (compress ? (lx + g.reach) >> 1 : lx + g.reach);
-        double mr = 0.0, sr = 0.0;
-        bool gathered = false;
 #pragma unroll 1
         for (int j = 0; j < 8; ++j) {
             const int qy = y + c_nbr2[j][1];
             if (qy < 0 || qy >= g.H) continue;  // K:407 rows skipped
-            const int qx = wrap_once(x + c_nbr2[j][0], g.W);  // K:410-413 columns wrap
-            const size_t qi = (size_t)qy * g.W + qx;
+            const size_t qi = (size_t)qy * g.W + wrap_once(x + c_nbr2[j][0], g.W);  // K:410-413 columns wrap
             const float d = depth_in[qi];
             const float nx = normal_in[3 * qi], ny = normal_in[3 * qi + 1], nz = normal_in[3 * qi + 2];
-            // K:418-432: skip exact duplicates of the best-so-far / of an already evaluated
-            // candidate.  Every earlier in-range neighbour was either evaluated or itself such a
-            // duplicate, so comparing with the original hypothesis and with the earlier
-            // neighbours (re-read through L1 instead of being kept in 32 registers) selects the
-            // same set, except that it also skips re-evaluating the original hypothesis once it
-            // has been displaced, which the strict < would reject anyway.
             bool dup = d == od && nx == onx && ny == ony && nz == onz;
             for (int m = 0; m < j; ++m) {
                 const int my = y + c_nbr2[m][1];
@@ -442,28 +451,74 @@ __global__ void __launch_bounds__(THREADS, D360_FAST_MINB)
                     dup = dup || (normal_in[3 * mi] == nx && normal_in[3 * mi + 1] == ny &&
                                   normal_in[3 * mi + 2] == nz);
             }
-            if (dup) continue;
-            if (!gathered) {
-                pixel_stats(g, t, ce, mr, sr);
-                gathered = true;
-            }
-            const double c = cand_cost<VT, float>(g, t, ce, mr, sr, d, nx, ny, nz);
-            ++evals;
+            if (!dup) mask |= 1u << j;
+        }
+    }
+    const int n_mine = __popc(mask);
+    if (n_mine) {
+        const int ce = (ly + g.reach) * t.wwc + (compress ? (lx + g.reach) >> 1 : lx + g.reach);
+        double mr, sr;
+        pixel_stats(g, t, ce, mr, sr);
+        q.stats[tid] = make_double2(mr, sr);
+    }
+    int incl = n_mine;  // CTA-wide exclusive scan of the counts
+    for (int o = 1; o < 32; o <<= 1) {
+        const int up = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((tid & 31) >= o) incl += up;
+    }
+    if ((tid & 31) == 31) q.warp_totals[tid >> 5] = incl;
+    __syncthreads();
+    int off = incl - n_mine;
+    for (int w = 0; w < (tid >> 5); ++w) off += q.warp_totals[w];
+    if (tid == THREADS - 1) q.total = off + n_mine;
+    for (unsigned m = mask; m; m &= m - 1) q.items[off++] = (unsigned short)(tid * 8 + (__ffs(m) - 1));
+    __syncthreads();
+
+    // ---- phase 2
+    const int total = q.total;
+    for (;;) {
+        int base = 0;
+        if ((tid & 31) == 0) base = atomicAdd(&q.next, 32);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base >= total) break;
+        const int it = base + (tid & 31);
+        if (it < total) {
+            const int item = q.items[it];
+            const int p = item >> 3, j = item & 7;
+            const int ply = p / (TW / 2);
+            const int py = y0 + ply;
+            const int plx = 2 * (p % (TW / 2)) + ((parity + py) & 1);
+            const int px = x0 + plx;
+            const size_t qi = (size_t)(py + c_nbr2[j][1]) * g.W + wrap_once(px + c_nbr2[j][0], g.W);
+            const int ce = (ply + g.reach) * t.wwc + (compress ? (plx + g.reach) >> 1 : plx + g.reach);
+            const double2 st = q.stats[p];
+            q.costs[item] = cand_cost<VT, float>(g, t, ce, st.x, st.y, depth_in[qi], normal_in[3 * qi],
+                                                 normal_in[3 * qi + 1], normal_in[3 * qi + 2]);
+        }
+    }
+    __syncthreads();
+
+    // ---- phase 3
+    if (live) {
+        double bc = (double)cost_in[i];
+        int bj = -1;
+        for (unsigned m = mask; m; m &= m - 1) {
+            const int j = __ffs(m) - 1;
+            const double c = q.costs[tid * 8 + j];
             if (c < bc) {  // K:463
                 bc = c;
-                bd = d; bnx = nx; bny = ny; bnz = nz;
+                bj = j;
             }
         }
-        depth_out[i] = bd;
-        normal_out[3 * i] = bnx;
-        normal_out[3 * i + 1] = bny;
-        normal_out[3 * i + 2] = bnz;
+        size_t bi = i;
+        if (bj >= 0) bi = (size_t)(y + c_nbr2[bj][1]) * g.W + wrap_once(x + c_nbr2[bj][0], g.W);
+        depth_out[i] = depth_in[bi];
+        normal_out[3 * i] = normal_in[3 * bi];
+        normal_out[3 * i + 1] = normal_in[3 * bi + 1];
+        normal_out[3 * i + 2] = normal_in[3 * bi + 2];
         cost_out[i] = (float)bc;
     }
-    if (n_evals != nullptr) {
-        for (int o = 16; o > 0; o >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, o);
-        if ((threadIdx.x & 31) == 0 && evals) atomicAdd(n_evals, (unsigned long long)evals);
-    }
+    if (n_evals != nullptr && tid == 0 && total) atomicAdd(n_evals, (unsigned long long)total);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -643,7 +698,7 @@ int fast_red_black(const GroupDev& gd, int parity, const float* di, const float*
                    float* nout, float* cout, unsigned long long* n_evals, cudaStream_t s) {
     FastGroup g;
     if (!make_fast_group(gd, &g)) return -1;
-    const size_t smem = tile_bytes(TW, TH_RB, g.reach, (g.stride & 1) == 0, gd.V);
+    const size_t smem = rb_queue_offset(tile_bytes(TW, TH_RB, g.reach, (g.stride & 1) == 0, gd.V)) + sizeof(RbQueue);
     if (smem > 200 * 1024) return -1;
     dim3 grid((gd.W + TW - 1) / TW, (gd.H + TH_RB - 1) / TH_RB);
     D360_FAST_DISPATCH(gd.V, {
