@@ -287,45 +287,56 @@ __device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, i
     for (int v = 0; v < VT; ++v) s0[v] = ss0[v] = rs0[v] = 0.0;
     bool bad = false;
 
-    const int half = (g.ns - 1) / 2;
-    int e_row = ce - half * (t.sx + t.sy);
-    for (int j = 0; j < g.ns; ++j) {
-        int e = e_row;
-        for (int i = 0; i < g.ns; ++i) {
-            const float4 q = t.qg[e];
-            double dn;
-            if constexpr (sizeof(HT) == 4) {
-                const float den = dot3_f32(nx, ny, nz, q.x, q.y, q.z);
-                bad = bad || (den > g.den_lim);
-                dn = (double)fminf(den, g.den_lim);
-            } else {
-                const double den = fma(nz, (double)q.z, fma(ny, (double)q.y, nx * (double)q.x));
-                const bool par = den > g.neg_par_eps;
-                bad = bad || par;
-                dn = par ? g.neg_par_eps : den;
-            }
-            const double lam = num * rcp3(dn);
-            const double rv = (double)q.w;
-            const double* rqe = t.rq + e;
-            {
-                double tx[VT], ty[VT], tz[VT], val[VT];
-#pragma unroll
-                for (int v = 0; v < VT; ++v) {
-                    tx[v] = fma(lam, rqe[(v * 3 + 0) * t.ne], g.rel_t[v][0]);
-                    ty[v] = fma(lam, rqe[(v * 3 + 1) * t.ne], g.rel_t[v][1]);
-                    tz[v] = fma(lam, rqe[(v * 3 + 2) * t.ne], g.rel_t[v][2]);
-                }
-                project_bilinear_all<VT>(g, tx, ty, tz, val);
-#pragma unroll
-                for (int v = 0; v < VT; ++v) {
-                    s0[v] += val[v];
-                    ss0[v] = fma(val[v], val[v], ss0[v]);
-                    rs0[v] = fma(rv, val[v], rs0[v]);
-                }
-            }
-            e += t.sx;
+    // lam_k = num / dn_k of sample k (K:240-247) and the f64 luma of that sample
+    auto plane_depth = [&](int e, double& lam, double& rv) {
+        const float4 q = t.qg[e];
+        double dn;
+        if constexpr (sizeof(HT) == 4) {
+            const float den = dot3_f32(nx, ny, nz, q.x, q.y, q.z);
+            bad = bad || (den > g.den_lim);
+            dn = (double)fminf(den, g.den_lim);
+        } else {
+            const double den = fma(nz, (double)q.z, fma(ny, (double)q.y, nx * (double)q.x));
+            const bool par = den > g.neg_par_eps;
+            bad = bad || par;
+            dn = par ? g.neg_par_eps : den;
         }
-        e_row += t.sy;
+        lam = num * rcp3(dn);
+        rv = (double)q.w;
+    };
+
+    // One flat loop over the S = ns * ns samples (dy outer, dx inner, E:60-65), software-pipelined
+    // by hand: the serial lam chain of sample k+1 (LDS, dot, rcp seed, Newton) is issued next to
+    // the VT projection chains of sample k instead of in front of them.
+    const int half = (g.ns - 1) / 2;
+    const int n_samples = g.ns * g.ns;
+    const int row_wrap = t.sy - g.ns * t.sx;
+    int e = ce - half * (t.sx + t.sy), col = 0;
+    double lam, rv;
+    plane_depth(e, lam, rv);
+    for (int k = 0; k < n_samples; ++k) {
+        int e_next = e + t.sx;
+        if (++col == g.ns) { col = 0; e_next += row_wrap; }
+        double lam_next = 0.0, rv_next = 0.0;
+        if (k + 1 < n_samples) plane_depth(e_next, lam_next, rv_next);
+        const double* rqe = t.rq + e;
+        double tx[VT], ty[VT], tz[VT], val[VT];
+#pragma unroll
+        for (int v = 0; v < VT; ++v) {
+            tx[v] = fma(lam, rqe[(v * 3 + 0) * t.ne], g.rel_t[v][0]);
+            ty[v] = fma(lam, rqe[(v * 3 + 1) * t.ne], g.rel_t[v][1]);
+            tz[v] = fma(lam, rqe[(v * 3 + 2) * t.ne], g.rel_t[v][2]);
+        }
+        project_bilinear_all<VT>(g, tx, ty, tz, val);
+#pragma unroll
+        for (int v = 0; v < VT; ++v) {
+            s0[v] += val[v];
+            ss0[v] = fma(val[v], val[v], ss0[v]);
+            rs0[v] = fma(rv, val[v], rs0[v]);
+        }
+        e = e_next;
+        lam = lam_next;
+        rv = rv_next;
     }
     if (bad) return trunc;
 
