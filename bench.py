@@ -12,7 +12,7 @@ keyframe sequence, no data-path collective -> weak scalin
 
 Prints ONE JSON line (rank 0).  `value` = keyframes of all ranks / max-over-ranks device
 time with the uint8 frames already resident in HBM; `e2e` = the same through the host-array
-API (numpy frames in pinned memory -> DepthStage.process -> consistency_filter -> numpy masks)
+streaming API (numpy frames in pinned memory -> StreamingDensifier.push -> numpy depth + mask)
 with the copies inside the timed region.
 
 `--impl reference` times the CPU restatement of the reference path (oracle/, C + pthreads,
@@ -230,38 +230,41 @@ def run_product(args) -> dict | None:
     _lib.trace_enable(False)
     n_evals_counted = int(stage.workspace.n_evals.item())
 
-    # ---- (B) end to end through the host-array API
-    stage_h = make_stage()
-    window_h = deque(maxlen=ccfg.window)
+    # ---- (B) end to end through the host-array streaming API: one pinned uint8 keyframe in per
+    # step (each keyframe is uploaded once and reused by the 5 groups it takes part in), one
+    # consistency-filtered depth map + mask out per step
+    stream = pipeline.StreamingDensifier(cam, spec, DEPTH_RANGE, iters, SEED, n_neighbors=V, warp=True,
+                                         consistency=ccfg, fusion=None, precision=args.precision,
+                                         init_rng="philox", device=dev)
+    fill = V + ccfg.window - 1  # pushes before the first output
+    n_push = fill + args.warmup + args.steps
+    fwd = list(range(SEQ_LEN))
+    cyc = fwd + fwd[-2:0:-1]
+    positions = [cyc[k % len(cyc)] for k in range(n_push)]
     bytes_in = bytes_out = 0
+    produced = 0
 
-    def step_host(i):
-        nonlocal bytes_in, bytes_out
+    def step_host(k):
+        nonlocal bytes_in, bytes_out, produced
         flush_buf.zero_()
-        g = group_of(i)
-        res = stage_h.process(g)  # numpy frames in, numpy depth + mask out
-        bytes_in += sum(k.image.nbytes for k in (g.reference, *g.neighbors))
-        bytes_out += res.pano.depth.nbytes + res.pano.valid.nbytes
-        window_h.append(res)
-        if len(window_h) == ccfg.window:
-            c = ccfg.window // 2
-            others = [(window_h[j].pano, window_h[j].pose) for j in range(ccfg.window) if j != c]
-            out = pipeline.consistency_filter(window_h[c].pano, window_h[c].pose, others, ccfg)
-            bytes_in += sum(q.depth.nbytes + q.valid.nbytes for q, _ in others) + \
-                window_h[c].pano.depth.nbytes + window_h[c].pano.valid.nbytes
-            bytes_out += out.valid.nbytes
-            return out
-        return res.pano
+        kf = p.Keyframe(id=k, image=host_imgs[positions[k]], pose=poses[positions[k]])
+        outs = stream.push(kf)  # numpy frame in, numpy depth + mask out
+        bytes_in += kf.image.nbytes
+        for o in outs:
+            bytes_out += o.pano.depth.nbytes + o.pano.valid.nbytes
+            produced += 1
 
-    for i in order[:args.warmup]:
-        step_host(i)
-    bytes_in = bytes_out = 0
+    for k in range(fill + args.warmup):
+        step_host(k)
+    bytes_in = bytes_out = produced = 0
     barrier()
     t0 = time.perf_counter()
-    for i in order[args.warmup:]:
-        step_host(i)
+    for k in range(fill + args.warmup, n_push):
+        step_host(k)
     barrier()
     e2e_s = time.perf_counter() - t0
+    if produced != args.steps:
+        raise SystemExit(f"streaming leg produced {produced} depth maps in {args.steps} steps")
 
     # ---- reduce over ranks
     times = torch.tensor([dev_ms, e2e_s * 1e3], dtype=torch.float64, device=dev)

@@ -28,7 +28,7 @@ _ENGINE_NAMES = {
 }
 _PIPELINE_NAMES = {
     "ConsistencyConfig", "FusionConfig", "FusedCloud", "DepthResult", "DeviceDepthResult", "DepthStage",
-    "consistency_filter", "FusionBuffer", "project_points", "POLE_LAT_LIMIT_DEG",
+    "consistency_filter", "FusionBuffer", "project_points", "POLE_LAT_LIMIT_DEG", "StreamingDensifier", "StreamOutput",
 }
 
 

@@ -264,11 +264,35 @@ def to_gray(image: np.ndarray) -> np.ndarray:
     return to_gray_device(image).cpu().numpy()
 
 
+class DeviceKeyframe:
+    """One keyframe's device-side planes, computed once and shared by every stereo group the
+    keyframe takes part in (as the reference or as a neighbour): uint8 image, dense f32 luma,
+    padded f32 luma and its f64 widening (layout of ``d360_group.nb`` / ``nb64``)."""
+
+    def __init__(self, image, camera: EquirectCamera, device=None):
+        self.device = _device(device)
+        h, w = camera.shape
+        with torch.cuda.device(self.device):
+            img = image if isinstance(image, torch.Tensor) else _up(np.asarray(image), np.uint8, self.device)
+            if tuple(img.shape[:2]) != (h, w):
+                raise ValueError(f"image {tuple(img.shape[:2])} does not match camera {(h, w)}")
+            self.image = img
+            self.gray = to_gray_device(img, self.device)
+            shape = (h + 2 * NB_PAD_Y, w + 2 * NB_PAD_X)
+            self.padded32 = torch.empty(shape, dtype=torch.float32, device=self.device)
+            self.padded64 = torch.empty(shape, dtype=torch.float64, device=self.device)
+            to_gray_device(img, self.device, out=self.padded32, pad=(NB_PAD_X, NB_PAD_Y), out64=self.padded64)
+
+
 class PreparedGroup:
-    """Stereo group unpacked into the kernel layout, resident on one GPU."""
+    """Stereo group unpacked into the kernel layout, resident on one GPU.
+
+    ``device_images``: optional uint8 CUDA tensors (reference first) instead of the keyframes'
+    host images; ``device_keyframes``: optional ``DeviceKeyframe`` list (reference first) whose
+    cached planes are gathered instead of recomputing the luma."""
 
     def __init__(self, group: StereoGroup, spec: PatchSpec, top_k: int | None = None,
-                 precision: str | None = None, device=None, device_images=None):
+                 precision: str | None = None, device=None, device_images=None, device_keyframes=None):
         self.group = group
         self.spec = spec
         self.camera = group.camera
@@ -285,20 +309,30 @@ class PreparedGroup:
             raise ConfigError(f"patch has {len(self.offsets)} samples; at most {_lib.MAX_SAMPLES} are supported")
         with torch.cuda.device(self.device):
             self.cam_dev = DeviceCamera.get(self.camera, self.device)
-            imgs = device_images if device_images is not None else (
-                [group.reference.image] + [nb.image for nb in group.neighbors])
-            ref_img = imgs[0] if isinstance(imgs[0], torch.Tensor) else _up(np.asarray(imgs[0]), np.uint8, self.device)
-            self.ref_image = ref_img  # u8 (H,W) / (H,W,3) on the device; fusion reads its colours
-            self.ref_gray = to_gray_device(ref_img, self.device)
             h, w = self.camera.shape
-            # neighbour luma planes, padded so that every bilinear footprint is in-plane (d360.h)
+            # neighbour luma planes, padded so that every bilinear footprint is in-plane (d360.h),
+            # and the same planes widened to f64: the reference interpolates in f64 (K:134-153)
             self.nb_padded = torch.empty((self.n_views, h + 2 * NB_PAD_Y, w + 2 * NB_PAD_X), dtype=torch.float32,
                                          device=self.device)
-            # the same planes widened to f64: the reference interpolates in f64 (K:134-153)
             self.nb64_padded = torch.empty(self.nb_padded.shape, dtype=torch.float64, device=self.device)
-            for v, im in enumerate(imgs[1:]):
-                to_gray_device(im, self.device, out=self.nb_padded[v], pad=(NB_PAD_X, NB_PAD_Y),
-                               out64=self.nb64_padded[v])
+            if device_keyframes is not None:
+                if len(device_keyframes) != self.n_views + 1:
+                    raise ValueError("device_keyframes must list the reference and every neighbour")
+                self.ref_image = device_keyframes[0].image
+                self.ref_gray = device_keyframes[0].gray
+                for v, dk in enumerate(device_keyframes[1:]):
+                    self.nb_padded[v].copy_(dk.padded32)
+                    self.nb64_padded[v].copy_(dk.padded64)
+            else:
+                imgs = device_images if device_images is not None else (
+                    [group.reference.image] + [nb.image for nb in group.neighbors])
+                ref_img = imgs[0] if isinstance(imgs[0], torch.Tensor) else _up(np.asarray(imgs[0]), np.uint8,
+                                                                                 self.device)
+                self.ref_image = ref_img  # u8 (H,W) / (H,W,3) on the device; fusion reads its colours
+                self.ref_gray = to_gray_device(ref_img, self.device)
+                for v, im in enumerate(imgs[1:]):
+                    to_gray_device(im, self.device, out=self.nb_padded[v], pad=(NB_PAD_X, NB_PAD_Y),
+                                   out64=self.nb64_padded[v])
         rel = [relative_transform(group.reference.pose, nb.pose) for nb in group.neighbors]
         self.rel_r = np.ascontiguousarray(np.stack([r for r, _ in rel]), dtype=np.float32)
         self.rel_t = np.ascontiguousarray(np.stack([t for _, t in rel]), dtype=np.float32)

@@ -20,6 +20,7 @@ from . import _lib
 from .engine import (
     DepthPanorama,
     DeviceCamera,
+    DeviceKeyframe,
     DeviceDepthPanorama,
     DevicePlaneMap,
     PatchMatchWorkspace,
@@ -316,3 +317,97 @@ class FusionBuffer:
                                             _ptr(colors), C.addressof(n_out), h, w, _stream()), "fuse_oldest")
             n = int(n_out.value)
             return DeviceFusedCloud(points[:n].clone(), colors[:n].clone(), oldest.id)
+
+
+# ---------------------------------------------------------------------------------------
+# streaming driver: keyframes in, filtered depth maps (and fused batches) out
+# ---------------------------------------------------------------------------------------
+
+def neighbor_order(n_views: int) -> list:
+    """Window offsets of the neighbours of the middle keyframe, nearest first, older before
+    newer: V=2 -> (-1, +1), the reference's triple; V=4 -> (-1, +1, -2, +2)."""
+    if n_views < 1 or n_views % 2:
+        raise ConfigError(f"the sliding keyframe window needs an even number of neighbours, got {n_views}")
+    order = []
+    for k in range(1, n_views // 2 + 1):
+        order += [-k, k]
+    return order
+
+
+@dataclass
+class StreamOutput:
+    """One finished keyframe of the stream: consistency-filtered depth map on the host, plus
+    the fused batch emitted at the same step (if fusion is enabled and its FIFO was full)."""
+
+    id: int
+    pano: DepthPanorama
+    pose: RigidPose
+    cloud: FusedCloud | None = None
+
+
+class StreamingDensifier:
+    """Stages of the reference's ``run_offline`` after the view filter, on one GPU:
+    sliding (V+1)-keyframe window with the middle frame as reference (``KeyframeBuffer``,
+    P:132-175, generalised from triples), ``DepthStage`` with warp carry-over, the consistency
+    window and optionally the fusion FIFO (``_ConsistencyFusion``).
+
+    Each keyframe is uploaded and converted once; depth maps stay in HBM between stages.  Per
+    ``push`` the host traffic is one uint8 frame in and (once the windows are full) one filtered
+    depth map + mask out."""
+
+    def __init__(self, camera: EquirectCamera, spec: PatchSpec, depth_range, iterations: int, seed: int,
+                 n_neighbors: int = 2, warp: bool = True, consistency: ConsistencyConfig | None = None,
+                 fusion: FusionConfig | None = None, median_window: int = 5, median_rel_threshold: float = 0.2,
+                 top_k: int | None = None, precision: str | None = None, init_rng: str = "pcg64", device=None,
+                 count_evals: bool = False):
+        self.camera = camera
+        self.order = neighbor_order(n_neighbors)
+        self.consistency = consistency if consistency is not None else ConsistencyConfig()
+        self.stage = DepthStage(camera, spec, depth_range, iterations, seed, warp=warp, median_window=median_window,
+                                median_rel_threshold=median_rel_threshold, top_k=top_k, precision=precision,
+                                init_rng=init_rng, device=device, count_evals=count_evals)
+        self.device = self.stage.device
+        self._frames: deque = deque(maxlen=n_neighbors + 1)  # (Keyframe, DeviceKeyframe)
+        self._window: deque = deque()                        # DeviceDepthResult
+        self._fusion = FusionBuffer(camera, fusion, self.device) if fusion is not None else None
+        self._last_id = None
+
+    def push(self, keyframe: Keyframe) -> list:
+        """Feed the next keyframe (ids strictly increasing); returns the outputs that
+        became final with it (0 or 1)."""
+        from .errors import OrderingError
+
+        if self._last_id is not None and keyframe.id <= self._last_id:
+            raise OrderingError(f"keyframe id {keyframe.id} arrived after id {self._last_id}; "
+                                "ids must be strictly increasing")
+        self._last_id = keyframe.id
+        self._frames.append((keyframe, DeviceKeyframe(keyframe.image, self.camera, self.device)))
+        if len(self._frames) < self._frames.maxlen:
+            return []
+        mid = len(self._frames) // 2
+        picks = [mid] + [mid + o for o in self.order]
+        group = StereoGroup(reference=self._frames[mid][0], neighbors=tuple(self._frames[i][0] for i in picks[1:]),
+                            camera=self.camera)
+        prep = PreparedGroup(group, self.stage.spec, top_k=self.stage.top_k, precision=self.stage.precision,
+                             device=self.device, device_keyframes=[self._frames[i][1] for i in picks])
+        self._window.append(self.stage.process_device(prep))
+        if len(self._window) < self.consistency.window:
+            return []
+        frames = list(self._window)
+        c = len(frames) // 2
+        target = frames[c]
+        others = [(f.pano, f.pose) for i, f in enumerate(frames) if i != c]
+        pano = consistency_filter_device(target.pano, target.pose, others, self.consistency)
+        self._window.popleft()
+        out = StreamOutput(target.id, pano.to_host(), target.pose)
+        if self._fusion is not None:
+            batch = self._fusion.push_device(DeviceDepthResult(target.id, pano, target.pose, target.image))
+            out.cloud = None if batch is None else batch.to_host()
+        return [out]
+
+    def finish(self) -> list:
+        """Flush the fusion FIFO; frames still inside the consistency window are
+        dropped, as in the reference."""
+        if self._fusion is None:
+            return []
+        return [b.to_host() for b in self._fusion.flush_device()]

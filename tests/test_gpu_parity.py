@@ -475,3 +475,54 @@ def test_c2_config_passes_vs_oracle(pkg, oracle):
     same2 = same & (got_d == rd)
     assert same2.mean() >= 1 - 2e-4
     assert cost_close(got_c[same2], rc[same2]).all()
+
+
+def test_streaming_densifier_matches_stagewise(pkg):
+    """StreamingDensifier (keyframes in, filtered maps + fused batches out) == the same stages
+    driven by hand, and its V=2 window is the reference's triple."""
+    p, engine, pipeline, synth = pkg
+    from paper_2211_16266_b200.errors import OrderingError
+
+    cam = p.EquirectCamera(64, 32)
+    scene = synth.default_scene("box")
+    kfs = []
+    for k in range(12):
+        pose = p.RigidPose(np.eye(3), np.array([0.05, 0.0, -0.55 + 0.1 * k]))
+        img, _ = synth.render_scene(scene, cam, pose)
+        kfs.append(p.Keyframe(id=k, image=img, pose=pose))
+    spec, dr = engine.PatchSpec(), (0.5, 8.0)
+    ccfg, fcfg = pipeline.ConsistencyConfig(), pipeline.FusionConfig()
+    sd = pipeline.StreamingDensifier(cam, spec, dr, 2, 3, n_neighbors=2, warp=True, consistency=ccfg, fusion=fcfg)
+    outs = []
+    for kf in kfs:
+        outs += sd.push(kf)
+    tail = sd.finish()
+    with pytest.raises(OrderingError):
+        sd.push(kfs[3])
+    # by hand
+    stage = pipeline.DepthStage(cam, spec, dr, 2, 3, warp=True)
+    fb = pipeline.FusionBuffer(cam, fcfg)
+    window, want, clouds = [], [], []
+    for i in range(1, 11):
+        g = p.StereoGroup(reference=kfs[i], neighbors=(kfs[i - 1], kfs[i + 1]), camera=cam)
+        window.append(stage.process_device(g))
+        if len(window) == 5:
+            c = window[2]
+            pano = pipeline.consistency_filter_device(c.pano, c.pose,
+                                                      [(w.pano, w.pose) for j, w in enumerate(window) if j != 2], ccfg)
+            want.append((c.id, pano.to_host()))
+            got = fb.push_device(pipeline.DeviceDepthResult(c.id, pano, c.pose, c.image))
+            clouds.append(None if got is None else got.to_host())
+            window.pop(0)
+    assert [o.id for o in outs] == [i for i, _ in want] == [3, 4, 5, 6, 7, 8]
+    for o, (_, w), cl in zip(outs, want, clouds):
+        assert np.array_equal(o.pano.depth, w.depth) and np.array_equal(o.pano.valid, w.valid)
+        assert (o.cloud is None) == (cl is None)
+        if cl is not None:
+            assert np.array_equal(o.cloud.points, cl.points) and np.array_equal(o.cloud.source_ids, cl.source_ids)
+    rest = fb.flush()
+    assert len(tail) == len(rest) and all(np.array_equal(a.points, b.points) for a, b in zip(tail, rest))
+    # V = 4 window: middle reference, neighbours nearest first
+    sd4 = pipeline.StreamingDensifier(cam, spec, dr, 1, 0, n_neighbors=4, warp=False, fusion=None)
+    n_out = sum(len(sd4.push(kf)) for kf in kfs)
+    assert n_out == len(kfs) - 4 - 4
