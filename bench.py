@@ -3,8 +3,9 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--workload c3]
 
-One "step" = one reference keyframe densified end to end on its GPU: luma conversion of the
-5 frames of the stereo group, plane-map warp from the previous keyframe + random fill,
+One "step" = one reference keyframe densified end to end on its GPU: luma planes of the
+keyframe that enters the sliding window (each keyframe is converted once and reused by the 5
+groups it takes part in), plane-map warp from the previous keyframe + random fill,
 eval + I x (red, black, refine) PatchMatch passes, median outlier filter, pole mask, and the
 geometric-consistency filter of the centre frame of the last 5 depth maps (BASELINE.json
 configs[2], "C3").  N > 1: one process per GPU (torchrun), every rank densifies its own
@@ -191,11 +192,21 @@ def run_product(args) -> dict | None:
     stage = make_stage()
     window = deque(maxlen=ccfg.window)
 
+    dk_cache = {}  # keyframe index -> DeviceKeyframe (planes computed once, on first use)
+
+    def device_keyframe(idx):
+        dk = dk_cache.get(idx)
+        if dk is None:
+            dk = dk_cache[idx] = engine.DeviceKeyframe(dev_imgs[idx], cam, dev)
+            for old in [k for k in dk_cache if abs(k - idx) > V]:
+                del dk_cache[old]
+        return dk
+
     def step_device(i):
         flush_buf.zero_()  # L2 flush (256 MiB > 126 MB L2), inside the timed region
         g = group_of(i)
         prep = engine.PreparedGroup(g, spec, precision=args.precision, device=dev,
-                                    device_images=[dev_imgs[i]] + [dev_imgs[i + o] for o in nb_order])
+                                    device_keyframes=[device_keyframe(i)] + [device_keyframe(i + o) for o in nb_order])
         res = stage.process_device(prep)
         window.append(res)
         if len(window) == ccfg.window:

@@ -60,10 +60,11 @@ typedef struct d360_group {
                                    (V,H,W).  d360_to_gray_padded writes this layout; pads >= 1
                                    enable the branch-free bilinear taps of the throughput kernels */
     int32_t nb_pad_x, nb_pad_y;
-    const double *nb64;         /* device, optional: the same padded planes widened to f64 (exact).
-                                   The reference interpolates in f64 (K:134-153); with f64 planes the
-                                   throughput kernels do so without per-tap conversions.  NULL: the
-                                   generic kernels run */
+    const double *nb64;         /* device, optional: the same padded planes widened to f64 (exact), two
+                                   doubles per texel: { value, value(x+1) - value }.  The reference
+                                   interpolates in f64 (K:134-153); with these planes a bilinear
+                                   footprint is two 16-byte loads and no per-tap conversion.
+                                   NULL: the generic kernels run */
     const float *rel_r;         /* host (V,3,3) x_nb = R x_ref + t (G:182-188), f32 (E:152) */
     const float *rel_t;         /* host (V,3) */
     const int32_t *offsets;     /* host (S,2) as (dx,dy) (E:60-65) */
@@ -121,8 +122,9 @@ int d360_median_support_mask(const float *depth, const uint8_t *valid, int half,
 /* replaces keyframes.to_gray (KF:64-72).  channels = 1 or 3, image device u8. */
 int d360_to_gray(const uint8_t *image, int channels, float *gray, int height, int width,
                  void *stream);
-/* same, written into the padded plane layout of d360_group.nb / nb64:
- * gray and gray64 (either may be NULL) are (height + 2*pad_y, width + 2*pad_x) */
+/* same, written into the padded plane layout of d360_group.nb / nb64: gray is
+ * (height + 2*pad_y, width + 2*pad_x) f32, gray64 the same raster with two doubles per texel
+ * { value, value(x+1) - value }; either may be NULL */
 int d360_to_gray_padded(const uint8_t *image, int channels, float *gray, double *gray64,
                         int height, int width, int pad_x, int pad_y, void *stream);
 

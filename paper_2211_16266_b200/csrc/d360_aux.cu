@@ -33,7 +33,10 @@ __global__ void k_to_gray(const uint8_t* __restrict__ img, int channels, float* 
     const int y = min(max(py - pad_y, 0), H - 1);
     const float l = luma_of(img, channels, (size_t)y * W + x);
     if (gray != nullptr) gray[(size_t)py * pw + px] = l;
-    if (gray64 != nullptr) gray64[(size_t)py * pw + px] = (double)l;
+    if (gray64 != nullptr) {  // { value, value(x+1) - value }
+        const float ln = luma_of(img, channels, (size_t)y * W + pos_mod(px + 1 - pad_x, W));
+        reinterpret_cast<double2*>(gray64)[(size_t)py * pw + px] = make_double2((double)l, (double)ln - (double)l);
+    }
 }
 
 // ---------------------------------------------------------------------------------------

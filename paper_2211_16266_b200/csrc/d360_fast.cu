@@ -38,7 +38,7 @@ struct FastGroup {
     size_t plane;         // elements per neighbour plane
     const float* rays;
     const float* ref_gray;
-    const double* nb64;   // padded planes widened to f64, see d360.h
+    const double* nb64;   // padded planes widened to f64, two doubles per texel, see d360.h
     float rel_r[D360_MAX_VIEWS][9];
     double rel_t[D360_MAX_VIEWS][3];
     double mu[8], cu[8];  // longitude: u = p * mu[oct] + cu[oct]
@@ -156,7 +156,8 @@ __device__ __forceinline__ double rsqrt3(double x, double c0375) {
 //
 // Bilinear: the planes are padded (wrapped columns, replicated rows), so floor(u), floor(u)+1,
 // floor(v), floor(v)+1 are all in-plane and the reference's wrap / clamp rules are data, not
-// code; they are stored widened to f64 so the taps need no conversion (an f32 lerp costs up to
+// code; they are stored widened to f64 as { value, value(x+1) - value }, so a footprint is two
+// 16-byte loads with no conversion and no subtraction (an f32 lerp costs up to
 // 1e-2 relative on the cost of low-texture patches, measured).  floor by the 1.5 * 2^23 magic
 // add; the element index is formed in f32 (exact below 2^23) and read out of the mantissa, so
 // no F2I / I2F conversions are issued; all offsets are 32-bit element indices from one base.
@@ -230,19 +231,18 @@ __device__ __forceinline__ void project_bilinear_all(const FastGroup& g, const d
         const float off = __fadd_rn(fmaf(fl_v[v], g.pitch_f, fl_u[v]), g.idx_bias);
         idx[v] = min((unsigned)__float_as_int(off) & 0x7fffffu, g.max_idx) + v * g.plane32;
     }
-    const double* __restrict__ nb = g.nb64;
-    double ta[VT], tb[VT], tc[VT], td[VT];
+    const double2* __restrict__ nb = reinterpret_cast<const double2*>(g.nb64);  // { value, value(x+1) - value }
+    double2 r0[VT], r1[VT];
 #pragma unroll
     D360_FORV {
-        ta[v] = __ldg(nb + idx[v]); tb[v] = __ldg(nb + idx[v] + 1u);
-        const unsigned idx1 = idx[v] + (unsigned)g.pitch;
-        tc[v] = __ldg(nb + idx1); td[v] = __ldg(nb + idx1 + 1u);
+        r0[v] = __ldg(nb + idx[v]);
+        r1[v] = __ldg(nb + (idx[v] + (unsigned)g.pitch));
     }
 #pragma unroll
     D360_FORV {
         const double fu = (double)(pu[v] - fl_u[v]), fv = (double)(pv[v] - fl_v[v]);
-        const double top = fma(tb[v] - ta[v], fu, ta[v]);
-        const double bot = fma(td[v] - tc[v], fu, tc[v]);
+        const double top = fma(r0[v].y, fu, r0[v].x);
+        const double bot = fma(r1[v].y, fu, r1[v].x);
         val[v] = fma(bot - top, fv, top);
     }
 }

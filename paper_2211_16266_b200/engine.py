@@ -231,8 +231,9 @@ def to_gray_device(image, device=None, out: torch.Tensor | None = None, pad=(0, 
 
     ``pad=(px, py)`` writes the padded plane layout of ``d360_group.nb``: shape
     (H + 2 py, W + 2 px) with wrapped columns and replicated rows.  ``out``: optional
-    contiguous float32 target of that shape; ``out64``: optional float64 target of the same
-    shape that receives the exactly widened values."""
+    contiguous float32 target of that shape; ``out64``: optional float64 target of shape
+    (..., 2) that receives, per texel, the exactly widened value and the difference to its right
+    neighbour (layout of ``d360_group.nb64``)."""
     dev = _device(device)
     lib = _lib.load()
     img = image if isinstance(image, torch.Tensor) else _up(np.asarray(image), np.uint8, dev)
@@ -252,9 +253,9 @@ def to_gray_device(image, device=None, out: torch.Tensor | None = None, pad=(0, 
         out = torch.empty(shape, dtype=torch.float32, device=dev)
     elif tuple(out.shape) != shape or out.dtype != torch.float32 or not out.is_contiguous():
         raise ValueError(f"out must be a contiguous float32 {shape} tensor")
-    if out64 is not None and (tuple(out64.shape) != shape or out64.dtype != torch.float64 or
+    if out64 is not None and (tuple(out64.shape) != (*shape, 2) or out64.dtype != torch.float64 or
                               not out64.is_contiguous()):
-        raise ValueError(f"out64 must be a contiguous float64 {shape} tensor")
+        raise ValueError(f"out64 must be a contiguous float64 {(*shape, 2)} tensor")
     _lib.check(lib.d360_to_gray_padded(_ptr(img), ch, _ptr(out), _ptr(out64), h, w, px, py, _stream()), "to_gray")
     return out
 
@@ -280,7 +281,7 @@ class DeviceKeyframe:
             self.gray = to_gray_device(img, self.device)
             shape = (h + 2 * NB_PAD_Y, w + 2 * NB_PAD_X)
             self.padded32 = torch.empty(shape, dtype=torch.float32, device=self.device)
-            self.padded64 = torch.empty(shape, dtype=torch.float64, device=self.device)
+            self.padded64 = torch.empty((*shape, 2), dtype=torch.float64, device=self.device)
             to_gray_device(img, self.device, out=self.padded32, pad=(NB_PAD_X, NB_PAD_Y), out64=self.padded64)
 
 
@@ -314,7 +315,7 @@ class PreparedGroup:
             # and the same planes widened to f64: the reference interpolates in f64 (K:134-153)
             self.nb_padded = torch.empty((self.n_views, h + 2 * NB_PAD_Y, w + 2 * NB_PAD_X), dtype=torch.float32,
                                          device=self.device)
-            self.nb64_padded = torch.empty(self.nb_padded.shape, dtype=torch.float64, device=self.device)
+            self.nb64_padded = torch.empty((*self.nb_padded.shape, 2), dtype=torch.float64, device=self.device)
             if device_keyframes is not None:
                 if len(device_keyframes) != self.n_views + 1:
                     raise ValueError("device_keyframes must list the reference and every neighbour")
