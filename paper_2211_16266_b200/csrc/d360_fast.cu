@@ -163,8 +163,9 @@ __device__ __forceinline__ double rsqrt3(double x, double c0375) {
 // no F2I / I2F conversions are issued; all offsets are 32-bit element indices from one base.
 #define D360_FORV for (int v = 0; v < VT; ++v)
 template <int VT>
-__device__ __forceinline__ void project_bilinear_all(const FastGroup& g, const double (&tx)[VT], const double (&ty)[VT],
-                                                     const double (&tz)[VT], double (&val)[VT]) {
+__device__ __forceinline__ void project_bilinear_all(const FastGroup& g, int v0, const double (&tx)[VT],
+                                                     const double (&ty)[VT], const double (&tz)[VT],
+                                                     double (&val)[VT]) {
     double r2[VT], y1[VT], e1[VT], a[VT], q[VT], w[VT], y2[VT], e2[VT], sq[VT];
 #pragma unroll
     D360_FORV r2[v] = fma(tz[v], tz[v], fma(ty[v], ty[v], fma(tx[v], tx[v], g.tiny)));
@@ -229,7 +230,7 @@ __device__ __forceinline__ void project_bilinear_all(const FastGroup& g, const d
 #pragma unroll
     D360_FORV {
         const float off = __fadd_rn(fmaf(fl_v[v], g.pitch_f, fl_u[v]), g.idx_bias);
-        idx[v] = min((unsigned)__float_as_int(off) & 0x7fffffu, g.max_idx) + v * g.plane32;
+        idx[v] = min((unsigned)__float_as_int(off) & 0x7fffffu, g.max_idx) + (unsigned)(v0 + v) * g.plane32;
     }
     const double2* __restrict__ nb = reinterpret_cast<const double2*>(g.nb64);  // { value, value(x+1) - value }
     double2 r0[VT], r1[VT];
@@ -320,19 +321,42 @@ __device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, i
         double lam_next = 0.0, rv_next = 0.0;
         if (k + 1 < n_samples) plane_depth(e_next, lam_next, rv_next);
         const double* rqe = t.rq + e;
-        double tx[VT], ty[VT], tz[VT], val[VT];
+        // views in chunks of at most 4 staged chains (more would not fit the register file)
+        constexpr int VC = VT <= 4 ? VT : (VT + 1) / 2;
 #pragma unroll
-        for (int v = 0; v < VT; ++v) {
-            tx[v] = fma(lam, rqe[(v * 3 + 0) * t.ne], g.rel_t[v][0]);
-            ty[v] = fma(lam, rqe[(v * 3 + 1) * t.ne], g.rel_t[v][1]);
-            tz[v] = fma(lam, rqe[(v * 3 + 2) * t.ne], g.rel_t[v][2]);
-        }
-        project_bilinear_all<VT>(g, tx, ty, tz, val);
+        for (int v0 = 0; v0 < VT; v0 += VC) {
+            if (v0 == 0) {
+                double tx[VC], ty[VC], tz[VC], val[VC];
 #pragma unroll
-        for (int v = 0; v < VT; ++v) {
-            s0[v] += val[v];
-            ss0[v] = fma(val[v], val[v], ss0[v]);
-            rs0[v] = fma(rv, val[v], rs0[v]);
+                for (int v = 0; v < VC; ++v) {
+                    tx[v] = fma(lam, rqe[(v * 3 + 0) * t.ne], g.rel_t[v][0]);
+                    ty[v] = fma(lam, rqe[(v * 3 + 1) * t.ne], g.rel_t[v][1]);
+                    tz[v] = fma(lam, rqe[(v * 3 + 2) * t.ne], g.rel_t[v][2]);
+                }
+                project_bilinear_all<VC>(g, 0, tx, ty, tz, val);
+#pragma unroll
+                for (int v = 0; v < VC; ++v) {
+                    s0[v] += val[v];
+                    ss0[v] = fma(val[v], val[v], ss0[v]);
+                    rs0[v] = fma(rv, val[v], rs0[v]);
+                }
+            } else {
+                constexpr int VR = VT - VC > 0 ? VT - VC : 1;  // second (last) chunk
+                double tx[VR], ty[VR], tz[VR], val[VR];
+#pragma unroll
+                for (int v = 0; v < VR; ++v) {
+                    tx[v] = fma(lam, rqe[((VC + v) * 3 + 0) * t.ne], g.rel_t[VC + v][0]);
+                    ty[v] = fma(lam, rqe[((VC + v) * 3 + 1) * t.ne], g.rel_t[VC + v][1]);
+                    tz[v] = fma(lam, rqe[((VC + v) * 3 + 2) * t.ne], g.rel_t[VC + v][2]);
+                }
+                project_bilinear_all<VR>(g, VC, tx, ty, tz, val);
+#pragma unroll
+                for (int v = 0; v < VR; ++v) {
+                    s0[VC + v] += val[v];
+                    ss0[VC + v] = fma(val[v], val[v], ss0[VC + v]);
+                    rs0[VC + v] = fma(rv, val[v], rs0[VC + v]);
+                }
+            }
         }
         e = e_next;
         lam = lam_next;
