@@ -526,3 +526,24 @@ def test_streaming_densifier_matches_stagewise(pkg):
     sd4 = pipeline.StreamingDensifier(cam, spec, dr, 1, 0, n_neighbors=4, warp=False, fusion=None)
     n_out = sum(len(sd4.push(kf)) for kf in kfs)
     assert n_out == len(kfs) - 4 - 4
+
+
+def test_run_patchmatch_end_to_end_v4_topk_vs_oracle(pkg, oracle):
+    """V = 4, top-k = 2 (unpinned by the reference; the oracle's per-view generalisation is the
+    yardstick): whole run from injected PCG64 hypotheses, statistical end-to-end gate."""
+    p, engine, _, synth = pkg
+    cam = p.EquirectCamera(256, 128)
+    group, gt = synth.make_group(synth.default_scene("box"), cam, n_views=4)
+    spec = engine.PatchSpec()
+    dr = (0.5, 16.0)
+    init = engine.random_init(engine.PlaneMap.empty(cam, dr), dr, seed=7)  # reference's PCG64 draws
+    pm, pano = engine.run_patchmatch(group, init, spec, 3, 7)
+    og = _oracle_group(oracle, group, 5, 2)
+    od, on, oc, ov = oracle.run_patchmatch(og, init.depth, init.normal, dr, 3, 7)
+    assert (pano.valid == ov).mean() >= 0.995
+    both = pano.valid & ov
+    ok = np.abs(pm.depth - od)[both] <= 0.005 * od[both]
+    assert ok.mean() >= 0.995, ok.mean()
+    same = (pm.depth == od) & (pm.normal == on).all(-1)
+    assert same.mean() >= 0.99  # in fact the trajectories stay identical almost everywhere
+    assert cost_close(pm.cost[same], oc[same]).all()
