@@ -60,9 +60,10 @@ struct RefineTable {
 // back to the generic kernels of d360_patchmatch.cu.
 int fast_eval(const struct GroupDev& gd, const float* depth, const float* normal, float* cost_out, cudaStream_t s);
 int fast_red_black(const struct GroupDev& gd, int parity, const float* di, const float* ni, const float* ci,
-                   float* dout, float* nout, float* cout, unsigned long long* n_evals, cudaStream_t s);
+                   float* dout, float* nout, float* cout, const unsigned char* changed_in,
+                   unsigned char* changed_out, unsigned long long* n_evals, cudaStream_t s);
 int fast_refine(const struct GroupDev& gd, const RefineTable& tab, float* depth, float* normal, float* cost,
-                unsigned long long* n_evals, cudaStream_t s);
+                unsigned char* changed, unsigned long long* n_evals, cudaStream_t s);
 
 void set_error(const char* fmt, ...);
 int check_launch(const char* what);

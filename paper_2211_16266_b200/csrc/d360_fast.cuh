@@ -1,0 +1,443 @@
+// Throughput build of the PatchMatch cost evaluation (precision policy D360_PREC_MIXED on a
+// regular sample grid) for sm_100a: shared device code of d360_fast_{eval,rb,refine}.cu.
+//
+// Same algorithm and same decision rules as d360_patchmatch.cu (K:156-297, K:300-610), with
+// the per-sample-view instruction stream cut to what the B200's pipes need:
+//   * FP64 pipe (64 lanes/clk/SM, DFMA latency 8 clk, the binding resource): ~50 operations
+//     per sample-view — t = lam * Rq + t_v, |t|^2, one third-order rsqrt / rcp refinement of
+//     the MUFU.64H seeds (error ~1e-18, no IEEE div/sqrt), the two degree-7 Horner chains of
+//     the reference's atan2 / acos polynomials, the f64 bilinear and the three NCC sums;
+//   * octant / hemisphere fix-ups of K:90-99 and K:129-131 are folded into one DFMA whose
+//     multiplier and addend come from 8- and 2-entry constant tables indexed by sign bits;
+//   * XU pipe (16 lanes/clk/SM): 3 MUFU.64H seeds + 4 F2F (u, v -> f32 as the reference's
+//     f32 scratch K:250-258, the exact f32 fractions -> f64); floor / frac of (u, v) use the
+//     1.5 * 2^23 magic-add on the FP32 pipe instead of F2I / I2F;
+//   * the patch geometry (samples per side, stride) is a template parameter for the
+//     reference's default patch, so every shared-memory offset is an immediate.
+// (u, v) are therefore the reference's f64 values to ~1e-12 px before the f32 rounding, which
+// is what holds the 1e-4 relative cost parity.
+//
+// One lane evaluates one hypothesis over all V views.  (Splitting an evaluation over a lane
+// pair, V / 2 views each, was built and measured: 80 registers and 3 CTAs per SM, but +25 %
+// instructions for the duplicated plane-depth chain and the per-lane view addressing, and the
+// smaller L1 next to 3 x 72 KB of shared memory: 20 % slower.  See DESIGN.md.)
+#pragma once
+#include <math.h>
+
+#include "d360_device.cuh"
+
+namespace d360 {
+namespace fast {
+
+constexpr int TW = 32;  // tile width (pixels)
+
+#ifndef D360_NT
+#define D360_NT 256  // threads per CTA
+#endif
+#ifndef D360_MINB
+#define D360_MINB 2  // CTAs per SM the register budget is sized for (128 registers)
+#endif
+
+struct FastGroup {
+    int W, H, ns, stride, reach, top_k;
+    int pitch;            // neighbour plane row pitch (W + 2 pad_x), elements
+    unsigned max_idx;     // last index of a plane from which a 2x2 footprint may start
+    size_t plane;         // elements per neighbour plane
+    const float* rays;
+    const float* ref_gray;
+    const double* nb64;   // padded planes widened to f64, two doubles per texel, see d360.h
+    float rel_r[D360_MAX_VIEWS][9];
+    double rel_t[D360_MAX_VIEWS][3];
+    double mu[8], cu[8];  // longitude: u = p * mu[oct] + cu[oct]
+    double mv[2], cv[2];  // latitude:  v = p * mv[hem] + cv[hem]
+    double ca[8], cq[8];  // atan / acos polynomial coefficients, highest degree first (K:75-85, K:112-122)
+    double trunc, inv_s;
+    double neg_par_eps, tiny, c0375;  // -PARALLEL_EPS, 1e-30 (K:246), 3/8: 64-bit literals live in the constant bank
+    unsigned plane32;     // plane as a 32-bit element count
+    float pitch_f;        // pitch as float
+    float idx_bias;       // 2^23 + pad_y * pitch + pad_x: float -> index by mantissa extraction
+    float den_lim;        // largest f32 below -PARALLEL_EPS
+};
+
+// V views, NS x NS samples at stride ST (NS = 0: taken from the FastGroup at run time).
+template <int V_, int NS_, int ST_>
+struct Cfg {
+    static constexpr int VT = V_, V = V_;
+    static constexpr int NT = D360_NT;
+    static constexpr int MINB = D360_MINB;
+    static constexpr int TH_FULL = NT / TW;    // eval / refine: NT pixels per CTA
+    static constexpr int TH_RB = 2 * NT / TW;  // red-black: NT pixels of the updated colour per CTA
+    static constexpr int NS = NS_, ST = ST_;
+    __host__ __device__ static int ns(const FastGroup& g) { return NS_ > 0 ? NS_ : g.ns; }
+    __host__ __device__ static int stride(const FastGroup& g) { return NS_ > 0 ? ST_ : g.stride; }
+    __host__ __device__ static int reach(const FastGroup& g) { return NS_ > 0 ? (NS_ - 1) / 2 * ST_ : g.reach; }
+};
+
+// Patch context of a CTA tile in shared memory.  Window entry (i, j) <-> pixel
+// ((x0 - R + i) mod W, clamp(y0 - R + j, 0, H-1)), K:168-177.  With `compress` (red-black pass
+// on an even sample stride: every sample of an updated pixel has the pixel's colour) only the
+// entries of that colour are kept, two window columns per slot — half the shared memory, and
+// neighbouring lanes read neighbouring slots.
+struct Tile {
+    const float4* qg;  // (qx, qy, qz, reference luma) per entry
+    const double* rq;  // [(v*3 + c) * ne + entry]  R_v q as f64 (exact widening of the f32 dot, K:184-189)
+    int wwc;           // entries per window row
+    int ne;            // entries per plane
+    int sx, sy;        // entry step of one sample column / row
+};
+
+__host__ __device__ inline int window_entries(int tw, int th, int reach, bool compress) {
+    const int ww = tw + 2 * reach;
+    return (compress ? ww / 2 : ww) * (th + 2 * reach);
+}
+__host__ __device__ inline size_t tile_bytes(int tw, int th, int reach, bool compress, int n_views) {
+    const size_t ne = (size_t)window_entries(tw, th, reach, compress);
+    return ne * sizeof(float4) + ne * sizeof(double) * 3 * n_views;
+}
+
+template <class C>
+__device__ __forceinline__ Tile tile_setup(const FastGroup& g, unsigned char* smem, int x0, int y0, int th,
+                                           bool compress, int keep) {
+    const int R = C::reach(g);
+    const int ww = TW + 2 * R, hh = th + 2 * R;
+    const int wwc = compress ? ww / 2 : ww;
+    const int ne = wwc * hh;
+    float4* qg = reinterpret_cast<float4*>(smem);
+    double* rq = reinterpret_cast<double*>(smem + (size_t)ne * sizeof(float4));
+    for (int e = threadIdx.x; e < ne; e += C::NT) {
+        const int j = e / wwc, ic = e - j * wwc;
+        const int i = compress ? 2 * ic + ((keep + j) & 1) : ic;
+        const int gx = pos_mod(x0 - R + i, g.W);
+        const int gy = min(max(y0 - R + j, 0), g.H - 1);
+        const size_t gi = (size_t)gy * g.W + gx;
+        const float bx = __ldg(g.rays + 3 * gi), by = __ldg(g.rays + 3 * gi + 1), bz = __ldg(g.rays + 3 * gi + 2);
+        qg[e] = make_float4(bx, by, bz, __ldg(g.ref_gray + gi));
+#pragma unroll
+        for (int v = 0; v < C::V; ++v) {
+            const float* r = g.rel_r[v];
+            rq[(v * 3 + 0) * ne + e] = (double)dot3_f32(r[0], r[1], r[2], bx, by, bz);
+            rq[(v * 3 + 1) * ne + e] = (double)dot3_f32(r[3], r[4], r[5], bx, by, bz);
+            rq[(v * 3 + 2) * ne + e] = (double)dot3_f32(r[6], r[7], r[8], bx, by, bz);
+        }
+    }
+    Tile t;
+    t.qg = qg;
+    t.rq = rq;
+    t.wwc = wwc;
+    t.ne = ne;
+    t.sx = compress ? C::stride(g) / 2 : C::stride(g);
+    t.sy = C::stride(g) * wwc;
+    return t;
+}
+
+// K:190-198 (f64 accumulation of the f32 luma and of its f32 square)
+template <class C>
+__device__ __forceinline__ void pixel_stats(const FastGroup& g, const Tile& t, int ce, double& mr, double& sr) {
+    double acc = 0.0, acc2 = 0.0;
+    const int ns = C::ns(g);
+    const int half = (ns - 1) / 2;
+    int e_row = ce - half * (t.sx + t.sy);
+#pragma unroll 1
+    for (int j = 0; j < ns; ++j) {
+        int e = e_row;
+#pragma unroll
+        for (int i = 0; i < ns; ++i) {
+            const float v = t.qg[e].w;
+            acc = __dadd_rn(acc, (double)v);
+            acc2 = __dadd_rn(acc2, (double)__fmul_rn(v, v));
+            e += t.sx;
+        }
+        e_row += t.sy;
+    }
+    const double m = acc * g.inv_s;  // S is a small integer: acc / S to <= 1 ulp, see note below
+    // the reference divides (acc / S); multiply-by-reciprocal differs by <= 1 ulp of f64,
+    // 12 orders below the parity tolerance.
+    double var = __dsub_rn(acc2 * g.inv_s, __dmul_rn(m, m));
+    var = var < 0.0 ? 0.0 : var;
+    mr = m;
+    sr = sqrt(var);
+}
+
+// 1/x, third-order refinement of the MUFU.RCP64H seed (2^-20 -> ~2^-60)
+__device__ __forceinline__ double rcp3(double x) {
+    const double y = rcp_seed(x);
+    const double e = fma(-x, y, 1.0);
+    return fma(y, fma(e, e, e), y);
+}
+
+// Stage A of one sample: (u, v) of K:244-258 for the VT neighbour-frame points, rounded to f32
+// like the reference's scratch.  Written stage by stage over the views so that the VT
+// independent dependency chains sit next to each other in program order.
+//
+// No guards on the two measure-zero singularities (t on the neighbour's polar axis:
+// max(|tx|,|tz|) = 0, or 1 - |ty|/|t| <= 0); they yield NaN, which the caller maps to `trunc`.
+#define D360_FORV for (int v = 0; v < VT; ++v)
+template <int VT>
+__device__ __forceinline__ void project_uv(const FastGroup& g, const double (&tx)[VT], const double (&ty)[VT],
+                                           const double (&tz)[VT], float (&pu)[VT], float (&pv)[VT]) {
+    double r2[VT], y1[VT], e1[VT], a[VT], q[VT], w[VT], y2[VT], e2[VT], sq[VT];
+#pragma unroll
+    D360_FORV r2[v] = fma(tz[v], tz[v], fma(ty[v], ty[v], fma(tx[v], tx[v], g.tiny)));
+#pragma unroll
+    D360_FORV y1[v] = rsqrt_seed(r2[v]);
+    double hi[VT], lo[VT], y3[VT];
+    bool swap[VT];
+#pragma unroll
+    D360_FORV {
+        swap[v] = fabs(tx[v]) > fabs(tz[v]);
+        hi[v] = swap[v] ? tx[v] : tz[v];
+        lo[v] = swap[v] ? tz[v] : tx[v];
+    }
+#pragma unroll
+    D360_FORV y3[v] = rcp_seed(hi[v]);
+#pragma unroll
+    D360_FORV e1[v] = fma(-(r2[v] * y1[v]), y1[v], 1.0);
+    double e3[VT];
+#pragma unroll
+    D360_FORV e3[v] = fma(-hi[v], y3[v], 1.0);
+#pragma unroll
+    D360_FORV y1[v] = fma(y1[v] * e1[v], fma(e1[v], g.c0375, 0.5), y1[v]);
+#pragma unroll
+    D360_FORV y3[v] = fma(y3[v], fma(e3[v], e3[v], e3[v]), y3[v]);
+#pragma unroll
+    D360_FORV a[v] = fabs(ty[v]) * y1[v];
+    double r[VT], s[VT], p[VT];
+#pragma unroll
+    D360_FORV { r[v] = lo[v] * y3[v]; s[v] = r[v] * r[v]; }
+#pragma unroll
+    D360_FORV { w[v] = 1.0 - a[v]; y2[v] = rsqrt_seed(w[v]); }
+#pragma unroll
+    D360_FORV { q[v] = g.cq[0]; p[v] = g.ca[0]; }
+#pragma unroll
+    for (int i = 1; i < 8; ++i) {
+#pragma unroll
+        D360_FORV { q[v] = fma(a[v], q[v], g.cq[i]); p[v] = fma(s[v], p[v], g.ca[i]); }
+    }
+    double s0[VT];
+#pragma unroll
+    D360_FORV { s0[v] = w[v] * y2[v]; e2[v] = fma(-s0[v], y2[v], 1.0); }
+#pragma unroll
+    D360_FORV sq[v] = fma(s0[v] * e2[v], fma(e2[v], g.c0375, 0.5), s0[v]);  // sqrt(w) = s0 (1 + e/2 + 3e^2/8)
+#pragma unroll
+    D360_FORV {
+        const unsigned hem = (unsigned)__double2hiint(ty[v]) >> 31;  // 1: ty < 0 (sphi > 0)
+        pv[v] = (float)fma(q[v] * sq[v], g.mv[hem], g.cv[hem]);
+        const unsigned hx = (unsigned)__double2hiint(tx[v]), hz = (unsigned)__double2hiint(tz[v]);
+        const unsigned oct = ((hx >> 31) * 2u + (hz >> 31)) * 2u + (swap[v] ? 1u : 0u);
+        pu[v] = (float)fma(fabs(r[v]) * p[v], g.mu[oct], g.cu[oct]);
+    }
+}
+
+// Stage B of one sample: the f64 bilinear taps of K:134-153 at the f32 (u, v) and the NCC sums.
+//
+// The planes are padded (wrapped columns, replicated rows), so floor(u), floor(u)+1, floor(v),
+// floor(v)+1 are all in-plane and the reference's wrap / clamp rules are data, not code; they
+// are stored widened to f64 as { value, value(x+1) - value }, so a footprint is two 16-byte
+// loads with no conversion and no subtraction (an f32 lerp costs up to 1e-2 relative on the
+// cost of low-texture patches, measured).  floor by the 1.5 * 2^23 magic add; the element index
+// is formed in f32 (exact below 2^23) and read out of the mantissa, so no F2I / I2F conversions
+// are issued; all offsets are 32-bit element indices from one base.
+template <int VT>
+__device__ __forceinline__ void gather_bilinear(const FastGroup& g, const double2* __restrict__ nb,
+                                                const float (&pu)[VT], const float (&pv)[VT], double (&val)[VT]) {
+    const float MAGIC = 12582912.0f;  // 1.5 * 2^23: (x + MAGIC) rounded towards -inf is floor(x) + MAGIC
+    float fl_u[VT], fl_v[VT];
+#pragma unroll
+    D360_FORV { fl_u[v] = __fadd_rn(__fadd_rd(pu[v], MAGIC), -MAGIC); fl_v[v] = __fadd_rn(__fadd_rd(pv[v], MAGIC), -MAGIC); }
+    unsigned idx[VT];
+#pragma unroll
+    D360_FORV {
+        const float off = __fadd_rn(fmaf(fl_v[v], g.pitch_f, fl_u[v]), g.idx_bias);
+        idx[v] = min((unsigned)__float_as_int(off) & 0x7fffffu, g.max_idx);
+    }
+    double2 r0[VT], r1[VT];  // { value, value(x+1) - value }
+#pragma unroll
+    D360_FORV {
+        const double2* __restrict__ row0 = nb + (size_t)v * g.plane32;  // uniform per view
+        const double2* __restrict__ row1 = row0 + g.pitch;
+        r0[v] = __ldg(row0 + idx[v]);
+        r1[v] = __ldg(row1 + idx[v]);
+    }
+#pragma unroll
+    D360_FORV {
+        const double fu = (double)(pu[v] - fl_u[v]), fv = (double)(pv[v] - fl_v[v]);
+        const double top = fma(r0[v].y, fu, r0[v].x);
+        const double bot = fma(r1[v].y, fu, r1[v].x);
+        val[v] = fma(bot - top, fv, top);
+    }
+}
+
+template <int NV>
+__device__ __forceinline__ double aggregate(double (&cv)[NV], int top_k) {
+#pragma unroll
+    for (int i = 1; i < NV; ++i) {
+#pragma unroll
+        for (int j = i; j > 0; --j) {
+            const double lo = cv[j - 1] < cv[j] ? cv[j - 1] : cv[j];
+            const double hi = cv[j - 1] < cv[j] ? cv[j] : cv[j - 1];
+            cv[j - 1] = lo;
+            cv[j] = hi;
+        }
+    }
+    double total = 0.0;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+        if (i < top_k) total = __dadd_rn(total, cv[i]);
+    return __dmul_rn(1.0 / top_k, total);
+}
+
+// Cost of one hypothesis at the pixel whose window entry is `ce` (K:201-297).
+template <class C, typename HT>
+__device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, int ce, double mr, double sr, HT d,
+                                            HT nx, HT ny, HT nz) {
+    constexpr int VT = C::VT;
+    const double trunc = g.trunc;
+    const float4 a = t.qg[ce];
+    double num;
+    if constexpr (sizeof(HT) == 4) {
+        const float ndota = dot3_f32(nx, ny, nz, a.x, a.y, a.z);
+        if ((double)ndota >= -D360_FACING_EPS || sr < D360_SIGMA_EPS) return trunc;
+        num = (double)__fmul_rn(d, ndota);
+    } else {
+        const double ndota = dot3_f64(nx, ny, nz, (double)a.x, (double)a.y, (double)a.z);
+        if (ndota >= -D360_FACING_EPS || sr < D360_SIGMA_EPS) return trunc;
+        num = __dmul_rn(d, ndota);
+    }
+    double s0[VT], ss0[VT], rs0[VT];
+#pragma unroll
+    for (int v = 0; v < VT; ++v) s0[v] = ss0[v] = rs0[v] = 0.0;
+    bool bad = false;
+    const double2* __restrict__ nb = reinterpret_cast<const double2*>(g.nb64);
+
+    // lam_k = num / dn_k of sample k (K:240-247) and the f64 luma of that sample
+    auto plane_depth = [&](int es, double& lam, double& rv) {
+        const float4 q = t.qg[es];
+        double dn;
+        if constexpr (sizeof(HT) == 4) {
+            const float den = dot3_f32(nx, ny, nz, q.x, q.y, q.z);
+            bad = bad || (den > g.den_lim);
+            dn = (double)fminf(den, g.den_lim);
+        } else {
+            const double den = fma(nz, (double)q.z, fma(ny, (double)q.y, nx * (double)q.x));
+            const bool par = den > g.neg_par_eps;
+            bad = bad || par;
+            dn = par ? g.neg_par_eps : den;
+        }
+        lam = num * rcp3(dn);
+        rv = (double)q.w;
+    };
+
+    // One flat loop over the S = ns * ns samples (dy outer, dx inner, E:60-65), software-pipelined
+    // by hand: the serial lam chain of sample k+1 (LDS, dot, rcp seed, Newton) is issued next to
+    // the projection chains of sample k instead of in front of them.  (Pipelining the gather of
+    // sample k against the projection of sample k+1 as well was measured: +3 % time, the
+    // 128-register budget has no room for it.)
+    const int ns = C::ns(g);
+    const int half = (ns - 1) / 2;
+    const int n_samples = ns * ns;
+    const int row_wrap = t.sy - ns * t.sx;
+    int e = ce - half * (t.sx + t.sy), col = 0;
+    double lam, rv;
+    plane_depth(e, lam, rv);
+#pragma unroll 1
+    for (int k = 0; k < n_samples; ++k) {
+        int e_next = e + t.sx;
+        if (++col == ns) { col = 0; e_next += row_wrap; }
+        double lam_next = 0.0, rv_next = 0.0;
+        if (k + 1 < n_samples) plane_depth(e_next, lam_next, rv_next);
+        const double* rqe = t.rq + e;
+        // at most 4 staged chains at a time (more would not fit the register file)
+        constexpr int VC = VT <= 4 ? VT : (VT + 1) / 2;
+#pragma unroll
+        for (int v0 = 0; v0 < VT; v0 += VC) {
+            if (v0 == 0) {
+                double tx[VC], ty[VC], tz[VC], val[VC];
+                float pu[VC], pv[VC];
+#pragma unroll
+                for (int v = 0; v < VC; ++v) {
+                    tx[v] = fma(lam, rqe[(v * 3 + 0) * t.ne], g.rel_t[v][0]);
+                    ty[v] = fma(lam, rqe[(v * 3 + 1) * t.ne], g.rel_t[v][1]);
+                    tz[v] = fma(lam, rqe[(v * 3 + 2) * t.ne], g.rel_t[v][2]);
+                }
+                project_uv<VC>(g, tx, ty, tz, pu, pv);
+                gather_bilinear<VC>(g, nb, pu, pv, val);
+#pragma unroll
+                for (int v = 0; v < VC; ++v) {
+                    s0[v] += val[v];
+                    ss0[v] = fma(val[v], val[v], ss0[v]);
+                    rs0[v] = fma(rv, val[v], rs0[v]);
+                }
+            } else {
+                constexpr int VR = VT - VC > 0 ? VT - VC : 1;  // second (last) chunk
+                double tx[VR], ty[VR], tz[VR], val[VR];
+                float pu[VR], pv[VR];
+#pragma unroll
+                for (int v = 0; v < VR; ++v) {
+                    tx[v] = fma(lam, rqe[((VC + v) * 3 + 0) * t.ne], g.rel_t[VC + v][0]);
+                    ty[v] = fma(lam, rqe[((VC + v) * 3 + 1) * t.ne], g.rel_t[VC + v][1]);
+                    tz[v] = fma(lam, rqe[((VC + v) * 3 + 2) * t.ne], g.rel_t[VC + v][2]);
+                }
+                project_uv<VR>(g, tx, ty, tz, pu, pv);
+                gather_bilinear<VR>(g, nb + (size_t)VC * g.plane32, pu, pv, val);
+#pragma unroll
+                for (int v = 0; v < VR; ++v) {
+                    s0[VC + v] += val[v];
+                    ss0[VC + v] = fma(val[v], val[v], ss0[VC + v]);
+                    rs0[VC + v] = fma(rv, val[v], rs0[VC + v]);
+                }
+            }
+        }
+        e = e_next;
+        lam = lam_next;
+        rv = rv_next;
+    }
+    if (bad) return trunc;
+
+    const double inv_s = g.inv_s;
+    double cv[VT];
+#pragma unroll
+    for (int v = 0; v < VT; ++v) {
+        cv[v] = trunc;
+        const double m0 = s0[v] * inv_s;
+        const double v0 = ss0[v] * inv_s - m0 * m0;
+        if (!(v0 < D360_VAR_EPS)) {
+            const double cov = rs0[v] * inv_s - mr * m0;
+            double c = 1.0 - cov / (sr * sqrt(v0));
+            c = c < 0.0 ? 0.0 : c;
+            c = c > trunc ? trunc : c;
+            cv[v] = c;
+        }
+    }
+    const double total = aggregate<VT>(cv, g.top_k);
+    return total == total ? total : trunc;  // NaN only from the unguarded polar singularities
+}
+
+// host side, d360_fast.cu
+bool make_fast_group(const GroupDev& gd, FastGroup* out);
+
+template <typename K>
+static int prepare(K kernel, size_t smem) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) {
+        set_error("cudaFuncSetAttribute(%zu B smem): %s", smem, cudaGetErrorString(e));
+        return 1;
+    }
+    return 0;
+}
+
+#define D360_FAST_GEO(V, ...)                                                         \
+    if (g.ns == 5 && g.stride == 2) { using C = Cfg<V, 5, 2>; __VA_ARGS__; }          \
+    else { using C = Cfg<V, 0, 0>; __VA_ARGS__; }
+
+#define D360_FAST_DISPATCH(V, ...)                                                    \
+    switch (V) {                                                                      \
+        case 1: D360_FAST_GEO(1, __VA_ARGS__) break;                                  \
+        case 2: D360_FAST_GEO(2, __VA_ARGS__) break;                                  \
+        case 3: D360_FAST_GEO(3, __VA_ARGS__) break;                                  \
+        case 4: D360_FAST_GEO(4, __VA_ARGS__) break;                                  \
+        case 6: D360_FAST_GEO(6, __VA_ARGS__) break;                                  \
+        default: return -1;                                                           \
+    }
+
+}  // namespace fast
+}  // namespace d360

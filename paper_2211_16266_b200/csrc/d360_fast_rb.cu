@@ -1,0 +1,203 @@
+// red_black_pass, K:352-473 (throughput build; see d360_fast.cuh).
+//
+// A CTA covers TW x TH_RB pixels, NT of them of the requested colour.  The number of candidates
+// a pixel has to evaluate varies (0..8 after the duplicate skipping of K:418-432), so the work
+// is levelled through a CTA-wide queue:
+//   phase 1  one thread per pixel: in-range, non-duplicate neighbours -> candidate mask;
+//            patch statistics; exclusive scan of the counts; (pixel, neighbour) items queued;
+//   phase 2  warps pull 32 items at a time and evaluate them (any lane, any pixel of the tile);
+//   phase 3  one thread per pixel: strict-< arg-min over its candidates in neighbour order
+//            (K:463; the cost of a hypothesis does not depend on evaluation order, so this is
+//            the reference's sequential accept).
+//
+// Unchanged-neighbour skipping (optional, `flags_in` / `flags_out`, one byte per pixel): a pixel p
+// that has itself not changed since its previous pass need not re-test the hypothesis of a
+// neighbour q that has not changed either.  The cost of a hypothesis at a pixel is a pure
+// function and acceptance is strict <: in the previous pass q's hypothesis was either evaluated
+// and not better than p's cost — which is still the same f32 value — or skipped as a duplicate
+// of p's own, still identical, hypothesis (K:418-432), or skipped by this rule, and then the
+// argument recurses.  The results are bit-identical; only evaluations are saved.  (p itself
+// must be unchanged: after a refinement accept the stored f32 hypothesis is not the f64 one its
+// stored cost was computed from, so "duplicate of my own hypothesis" no longer implies "not
+// better than my cost" once p moves on; and a cost that was stored after rounding up lets the
+// reference accept an equal-cost candidate, e.g. at the truncation cost, f32(1.2) > 1.2.)
+//   flag = 1: the pixel's hypothesis changed during its own red-black pass or the refinement
+//   of the previous iteration.  The first iteration starts from all ones.  A pass writes
+//   flags_out for the pixels it updates and refine_pass sets it where it accepts.  All eight
+//   neighbours have the pixel's colour, so a pass reads only flags that no pass of the same
+//   iteration writes.
+#include "d360_fast.cuh"
+
+namespace d360 {
+namespace fast {
+
+__constant__ int c_nbr2[8][2] = {{-1, -1}, {1, -1}, {-1, 1}, {1, 1}, {0, -2}, {0, 2}, {-2, 0}, {2, 0}};
+
+template <int NT>
+struct RbQueue {
+    double2 stats[NT];            // (mr, sr) per pixel
+    double costs[NT * 8];         // cost of neighbour j's hypothesis at pixel p
+    unsigned short items[NT * 8]; // p * 8 + j
+    int warp_totals[NT / 32];
+    int total, next;
+};
+
+__host__ __device__ inline size_t rb_queue_offset(size_t tile) { return (tile + 15) & ~(size_t)15; }
+
+template <class C>
+__global__ void __launch_bounds__(C::NT, C::MINB)
+    k_red_black(const __grid_constant__ FastGroup g, int parity, const float* __restrict__ depth_in,
+                const float* __restrict__ normal_in, const float* __restrict__ cost_in, float* __restrict__ depth_out,
+                float* __restrict__ normal_out, float* __restrict__ cost_out,
+                const unsigned char* __restrict__ flags_in, unsigned char* __restrict__ flags_out,
+                unsigned long long* n_evals) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int NT = C::NT;
+    const int x0 = blockIdx.x * TW, y0 = blockIdx.y * C::TH_RB;  // x0 is even
+    const int R = C::reach(g);
+    const bool compress = (C::stride(g) & 1) == 0;
+    RbQueue<NT>& q = *reinterpret_cast<RbQueue<NT>*>(smem + rb_queue_offset(tile_bytes(TW, C::TH_RB, R, compress, C::V)));
+    if (threadIdx.x == 0) q.next = 0;
+    const Tile t = tile_setup<C>(g, smem, x0, y0, C::TH_RB, compress, (parity + y0) & 1);
+    __syncthreads();
+
+    // ---- phase 1
+    const int tid = threadIdx.x;
+    const int ly = tid / (TW / 2);
+    const int y = y0 + ly;
+    const int lx = 2 * (tid % (TW / 2)) + ((parity + y) & 1);
+    const int x = x0 + lx;
+    const bool live = x < g.W && y < g.H;
+    if (y < g.H) {
+        // carry the off-colour pixel of this pair over unchanged (E:575-577)
+        const int xo = x0 + (lx ^ 1);
+        if (xo < g.W) {
+            const size_t o = (size_t)y * g.W + xo;
+            depth_out[o] = depth_in[o];
+            normal_out[3 * o] = normal_in[3 * o];
+            normal_out[3 * o + 1] = normal_in[3 * o + 1];
+            normal_out[3 * o + 2] = normal_in[3 * o + 2];
+            cost_out[o] = cost_in[o];
+        }
+    }
+    const size_t i = live ? (size_t)y * g.W + x : 0;
+    unsigned mask = 0;
+    if (live) {
+        // K:418-432 skips exact duplicates of the best-so-far and of already evaluated
+        // candidates.  Every earlier in-range neighbour was either evaluated or itself such a
+        // duplicate, so comparing with the pixel's original hypothesis and with the earlier
+        // neighbours selects the same set, except that it also skips re-evaluating the original
+        // hypothesis once it has been displaced, which strict < would reject anyway.
+        const bool may_skip = flags_in != nullptr && flags_in[i] == 0;
+        const float od = depth_in[i];
+        const float onx = normal_in[3 * i], ony = normal_in[3 * i + 1], onz = normal_in[3 * i + 2];
+#pragma unroll 1
+        for (int j = 0; j < 8; ++j) {
+            const int qy = y + c_nbr2[j][1];
+            if (qy < 0 || qy >= g.H) continue;  // K:407 rows skipped
+            const size_t qi = (size_t)qy * g.W + wrap_once(x + c_nbr2[j][0], g.W);  // K:410-413 columns wrap
+            const float d = depth_in[qi];
+            const float nx = normal_in[3 * qi], ny = normal_in[3 * qi + 1], nz = normal_in[3 * qi + 2];
+            bool dup = d == od && nx == onx && ny == ony && nz == onz;
+            for (int m = 0; m < j; ++m) {
+                const int my = y + c_nbr2[m][1];
+                if (my < 0 || my >= g.H) continue;
+                const size_t mi = (size_t)my * g.W + wrap_once(x + c_nbr2[m][0], g.W);
+                if (depth_in[mi] == d)
+                    dup = dup || (normal_in[3 * mi] == nx && normal_in[3 * mi + 1] == ny &&
+                                  normal_in[3 * mi + 2] == nz);
+            }
+            if (!dup && (!may_skip || flags_in[qi])) mask |= 1u << j;
+        }
+    }
+    const int n_mine = __popc(mask);
+    if (n_mine) {
+        const int ce = (ly + R) * t.wwc + (compress ? (lx + R) >> 1 : lx + R);
+        double mr, sr;
+        pixel_stats<C>(g, t, ce, mr, sr);
+        q.stats[tid] = make_double2(mr, sr);
+    }
+    int incl = n_mine;  // CTA-wide exclusive scan of the counts
+    for (int o = 1; o < 32; o <<= 1) {
+        const int up = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((tid & 31) >= o) incl += up;
+    }
+    if ((tid & 31) == 31) q.warp_totals[tid >> 5] = incl;
+    __syncthreads();
+    int off = incl - n_mine;
+    for (int w = 0; w < (tid >> 5); ++w) off += q.warp_totals[w];
+    if (tid == NT - 1) q.total = off + n_mine;
+    for (unsigned m = mask; m; m &= m - 1) q.items[off++] = (unsigned short)(tid * 8 + (__ffs(m) - 1));
+    __syncthreads();
+
+    // ---- phase 2
+    const int total = q.total;
+    for (;;) {
+        int base = 0;
+        if ((tid & 31) == 0) base = atomicAdd(&q.next, 32);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base >= total) break;
+        const int it = base + (tid & 31);
+        if (it < total) {
+            const int item = q.items[it];
+            const int p = item >> 3, j = item & 7;
+            const int ply = p / (TW / 2);
+            const int py = y0 + ply;
+            const int plx = 2 * (p % (TW / 2)) + ((parity + py) & 1);
+            const int px = x0 + plx;
+            const size_t qi = (size_t)(py + c_nbr2[j][1]) * g.W + wrap_once(px + c_nbr2[j][0], g.W);
+            const int ce = (ply + R) * t.wwc + (compress ? (plx + R) >> 1 : plx + R);
+            const double2 st = q.stats[p];
+            q.costs[item] = cand_cost<C, float>(g, t, ce, st.x, st.y, depth_in[qi], normal_in[3 * qi],
+                                                normal_in[3 * qi + 1], normal_in[3 * qi + 2]);
+        }
+    }
+    __syncthreads();
+
+    // ---- phase 3
+    if (live) {
+        double bc = (double)cost_in[i];
+        int bj = -1;
+        for (unsigned m = mask; m; m &= m - 1) {
+            const int j = __ffs(m) - 1;
+            const double c = q.costs[tid * 8 + j];
+            if (c < bc) {  // K:463
+                bc = c;
+                bj = j;
+            }
+        }
+        size_t bi = i;
+        if (bj >= 0) bi = (size_t)(y + c_nbr2[bj][1]) * g.W + wrap_once(x + c_nbr2[bj][0], g.W);
+        depth_out[i] = depth_in[bi];
+        normal_out[3 * i] = normal_in[3 * bi];
+        normal_out[3 * i + 1] = normal_in[3 * bi + 1];
+        normal_out[3 * i + 2] = normal_in[3 * bi + 2];
+        cost_out[i] = (float)bc;
+        if (flags_out != nullptr) flags_out[i] = bj >= 0;
+    }
+    if (n_evals != nullptr && tid == 0 && total) atomicAdd(n_evals, (unsigned long long)total);
+}
+
+}  // namespace fast
+
+using namespace fast;
+
+int fast_red_black(const GroupDev& gd, int parity, const float* di, const float* ni, const float* ci, float* dout,
+                   float* nout, float* cout, const unsigned char* flags_in, unsigned char* flags_out,
+                   unsigned long long* n_evals, cudaStream_t s) {
+    FastGroup g;
+    if (!make_fast_group(gd, &g)) return -1;
+    D360_FAST_DISPATCH(gd.V, {
+        const size_t smem = rb_queue_offset(tile_bytes(TW, C::TH_RB, g.reach, (g.stride & 1) == 0, gd.V)) +
+                            sizeof(RbQueue<C::NT>);
+        if (smem > 200 * 1024) return -1;
+        dim3 grid((gd.W + TW - 1) / TW, (gd.H + C::TH_RB - 1) / C::TH_RB);
+        auto k = k_red_black<C>;
+        if (prepare(k, smem)) return 1;
+        TraceScope ts_("red_black", s);
+        k<<<grid, C::NT, smem, s>>>(g, parity, di, ni, ci, dout, nout, cout, flags_in, flags_out, n_evals);
+    })
+    return check_launch("red_black_pass");
+}
+
+}  // namespace d360

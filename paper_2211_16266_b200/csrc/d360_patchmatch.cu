@@ -459,12 +459,20 @@ static int launch_eval(const GroupDev& gd, int prec, const float* depth, const f
     return rc ? rc : check_launch("eval_costs");
 }
 
+// changed_in / changed_out (optional): unchanged-neighbour skipping of the throughput kernels
+// (d360_fast_rb.cu).  The generic kernels do not use the flags; they mark every pixel changed,
+// which is always safe.
 static int launch_red_black(const GroupDev& gd, int prec, int parity, const float* di,
                             const float* ni, const float* ci, float* dout, float* nout, float* cout,
+                            const unsigned char* changed_in, unsigned char* changed_out,
                             unsigned long long* n_evals, cudaStream_t s) {
     if (prec == D360_PREC_MIXED) {
-        const int frc = fast_red_black(gd, parity, di, ni, ci, dout, nout, cout, n_evals, s);
+        const int frc = fast_red_black(gd, parity, di, ni, ci, dout, nout, cout, changed_in, changed_out, n_evals, s);
         if (frc >= 0) return frc;
+    }
+    if (changed_out != nullptr && cudaMemsetAsync(changed_out, 1, (size_t)gd.W * gd.H, s) != cudaSuccess) {
+        set_error("cudaMemsetAsync(changed flags) failed");
+        return 1;
     }
     const size_t smem = tile_smem_bytes(TILE_W, TILE_H, gd.reach, gd.V);
     dim3 grid((gd.W + TILE_W - 1) / TILE_W, (gd.H + TILE_H - 1) / TILE_H);
@@ -481,10 +489,15 @@ static int launch_red_black(const GroupDev& gd, int prec, int parity, const floa
 }
 
 static int launch_refine(const GroupDev& gd, int prec, const RefineTable& tab, float* depth,
-                         float* normal, float* cost, unsigned long long* n_evals, cudaStream_t s) {
+                         float* normal, float* cost, unsigned char* changed, unsigned long long* n_evals,
+                         cudaStream_t s) {
     if (prec == D360_PREC_MIXED) {
-        const int frc = fast_refine(gd, tab, depth, normal, cost, n_evals, s);
+        const int frc = fast_refine(gd, tab, depth, normal, cost, changed, n_evals, s);
         if (frc >= 0) return frc;
+    }
+    if (changed != nullptr && cudaMemsetAsync(changed, 1, (size_t)gd.W * gd.H, s) != cudaSuccess) {
+        set_error("cudaMemsetAsync(changed flags) failed");
+        return 1;
     }
     const size_t smem = tile_smem_bytes(TILE_W, TILE_H, gd.reach, gd.V);
     dim3 grid((gd.W + TILE_W - 1) / TILE_W, (gd.H + TILE_H - 1) / TILE_H);
@@ -545,7 +558,7 @@ extern "C" int d360_red_black_pass(const d360_group* g, int parity, const float*
         return 1;
     }
     return launch_red_black(gd, g->precision, parity, depth_in, normal_in, cost_in, depth_out,
-                            normal_out, cost_out, n_evals, (cudaStream_t)stream);
+                            normal_out, cost_out, nullptr, nullptr, n_evals, (cudaStream_t)stream);
 }
 
 extern "C" int d360_refine_pass(const d360_group* g, float* depth, float* normal, float* cost,
@@ -557,12 +570,13 @@ extern "C" int d360_refine_pass(const d360_group* g, float* depth, float* normal
     RefineTable tab;
     if (fill_table(&tab, cand_dd, cand_sa, cand_ca, cand_caz, cand_saz, n_cand, depth_min, depth_max))
         return 1;
-    return launch_refine(gd, g->precision, tab, depth, normal, cost, nullptr, (cudaStream_t)stream);
+    return launch_refine(gd, g->precision, tab, depth, normal, cost, nullptr, nullptr, (cudaStream_t)stream);
 }
 
 extern "C" int d360_run_patchmatch(const d360_group* g, float* depth, float* normal, float* cost,
                                    float* scratch_depth, float* scratch_normal, float* scratch_cost,
-                                   const float* tables, int iterations, int n_cand, double depth_min,
+                                   uint8_t* scratch_changed, const float* tables, int iterations, int n_cand,
+                                   double depth_min,
                                    double depth_max, uint8_t* valid_out, unsigned long long* n_evals,
                                    void* stream) {
     GroupDev gd;
@@ -576,9 +590,17 @@ extern "C" int d360_run_patchmatch(const d360_group* g, float* depth, float* nor
     if (launch_eval(gd, prec, depth, normal, cost, s)) return 1;
     float *cd = depth, *cn = normal, *cc = cost;
     float *nd = scratch_depth, *nn = scratch_normal, *nc = scratch_cost;
+    // unchanged-neighbour skipping: two flag planes, read one / write the other, swapped per iteration
+    const size_t n_px = (size_t)gd.W * gd.H;
+    unsigned char* chg_in = scratch_changed;
+    unsigned char* chg_out = scratch_changed != nullptr ? scratch_changed + n_px : nullptr;
+    if (chg_in != nullptr && cudaMemsetAsync(chg_in, 1, n_px, s) != cudaSuccess) {
+        set_error("cudaMemsetAsync(changed flags) failed");
+        return 1;
+    }
     for (int it = 0; it < iterations; ++it) {
         for (int parity = 0; parity < 2; ++parity) {
-            if (launch_red_black(gd, prec, parity, cd, cn, cc, nd, nn, nc, n_evals, s)) return 1;
+            if (launch_red_black(gd, prec, parity, cd, cn, cc, nd, nn, nc, chg_in, chg_out, n_evals, s)) return 1;
             float* tmp;
             tmp = cd; cd = nd; nd = tmp;
             tmp = cn; cn = nn; nn = tmp;
@@ -590,10 +612,11 @@ extern "C" int d360_run_patchmatch(const d360_group* g, float* depth, float* nor
         if (fill_table(&tab, tb, tb + n_cand, tb + 2 * n_cand, tb + 3 * n_cand, tb + 4 * n_cand, n_cand,
                        depth_min, depth_max))
             return 1;
-        if (launch_refine(gd, prec, tab, cd, cn, cc, n_evals, s)) return 1;
+        if (launch_refine(gd, prec, tab, cd, cn, cc, chg_out, n_evals, s)) return 1;
+        unsigned char* tmpc = chg_in; chg_in = chg_out; chg_out = tmpc;
     }
     if (valid_out != nullptr) {
-        const size_t n = (size_t)gd.W * gd.H;
+        const size_t n = n_px;
         {
             TraceScope ts_("valid_from_cost", s);
             k_valid_from_cost<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(cc, (float)gd.trunc, valid_out, n);

@@ -517,6 +517,7 @@ class PatchMatchWorkspace:
         self.depth = torch.empty((h, w), dtype=torch.float32, device=device)
         self.normal = torch.empty((h, w, 3), dtype=torch.float32, device=device)
         self.cost = torch.empty((h, w), dtype=torch.float32, device=device)
+        self.changed = torch.empty((2, h, w), dtype=torch.uint8, device=device)
         self.n_evals = torch.zeros((1,), dtype=torch.int64, device=device)
 
 
@@ -524,12 +525,14 @@ def run_patchmatch_device(prep: PreparedGroup, pm: DevicePlaneMap, iterations: i
                           refine_theta_deg: float = DEFAULT_REFINE_THETA_DEG,
                           refine_depth_fraction: float = DEFAULT_REFINE_DEPTH_FRACTION,
                           workspace: PatchMatchWorkspace | None = None, count_evals: bool = False,
-                          check_valid: bool = True):
+                          check_valid: bool = True, skip_unchanged: bool = True):
     """Optimise ``pm`` in place on the device; returns (pm, DeviceDepthPanorama).
 
     One C-ABI call (d360_run_patchmatch) enqueues eval + iterations x (red, black, refine).
     With ``count_evals`` the executed propagation/refinement cost evaluations are ADDED to
-    ``workspace.n_evals`` (zero it yourself; reading it synchronises)."""
+    ``workspace.n_evals`` (zero it yourself; reading it synchronises).  ``skip_unchanged`` lets a
+    pixel skip re-testing neighbour hypotheses that did not change since the previous iteration
+    (result-neutral, see include/d360.h); switch it off to count the reference's evaluations."""
     if iterations < 1:
         raise ConfigError(f"patchmatch.iterations must be >= 1, got {iterations}")
     if prep.camera != pm.camera:
@@ -544,7 +547,8 @@ def run_patchmatch_device(prep: PreparedGroup, pm: DevicePlaneMap, iterations: i
     with torch.cuda.device(prep.device):
         valid = torch.empty(prep.camera.shape, dtype=torch.uint8, device=prep.device)
         _lib.check(lib.d360_run_patchmatch(prep.struct, _ptr(pm.depth), _ptr(pm.normal), _ptr(pm.cost),
-                                           _ptr(ws.depth), _ptr(ws.normal), _ptr(ws.cost), tables.ctypes.data,
+                                           _ptr(ws.depth), _ptr(ws.normal), _ptr(ws.cost),
+                                           _ptr(ws.changed) if skip_unchanged else 0, tables.ctypes.data,
                                            int(iterations), REFINE_CANDIDATES, float(dmin), float(dmax),
                                            _ptr(valid), _ptr(ws.n_evals) if count_evals else 0, _stream()),
                    "run_patchmatch")

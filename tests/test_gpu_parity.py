@@ -192,6 +192,56 @@ def test_run_patchmatch_deterministic_and_argchecks(pkg):
 
 
 @pytest.mark.parametrize("precision", PRECISIONS)
+@pytest.mark.parametrize("name,iterations", [("hot_256x128_c1", 6), ("hot_64x32_rot", 4)])
+def test_unchanged_neighbour_skipping_is_result_neutral(pkg, name, iterations, precision):
+    """Skipping re-tests of neighbour hypotheses that did not change since the previous
+    iteration must not change a single bit of the result (a re-test is always rejected by the
+    strict < of K:463); it only removes evaluations."""
+    p, engine, _, _ = pkg
+    z = load_golden(name)
+    group, spec, cam = make_group(p, z)
+    prep = engine.prepare_group(group, spec, precision=precision)
+    init = engine.PlaneMap(cam, z["init_depth"], z["init_normal"], np.full(cam.shape, np.inf, np.float32),
+                           np.ones(cam.shape, bool), tuple(z["depth_range"]))
+    out, evals = {}, {}
+    for skip in (False, True):
+        ws = engine.PatchMatchWorkspace(cam, prep.device)
+        pm = engine.DevicePlaneMap.from_host(init)
+        engine.run_patchmatch_device(prep, pm, iterations, int(z["seed"]), workspace=ws, count_evals=True,
+                                     skip_unchanged=skip)
+        out[skip] = (pm.depth.cpu().numpy(), pm.normal.cpu().numpy(), pm.cost.cpu().numpy())
+        evals[skip] = int(ws.n_evals.item())
+    for a, b in zip(out[False], out[True]):
+        assert np.array_equal(a, b)
+    assert evals[True] <= evals[False]
+    if precision == "mixed":  # the throughput kernels implement the skip; the literal ones ignore the flags
+        assert evals[True] < evals[False], evals
+
+
+def test_unchanged_neighbour_skipping_full_size(pkg):
+    """Same, at 960x480 with 4 views from a Philox start.  Two cases need the rule "the pixel itself
+    is unchanged too": pixels at the truncation cost, where the reference keeps swapping equal-cost
+    hypotheses (f32(1.2) > 1.2), and pixels whose stored cost belongs to the unrounded f64
+    hypothesis of a refinement accept (a skip rule without it differs on ~1 pixel per map)."""
+    p, engine, _, synth = pkg
+    cam = p.EquirectCamera(960, 480)
+    group, _ = synth.make_group(synth.default_scene("box"), cam, n_views=4)
+    prep = engine.prepare_group(group, engine.PatchSpec(), precision="mixed")
+    out, evals = {}, {}
+    for skip in (False, True):
+        ws = engine.PatchMatchWorkspace(cam, prep.device)
+        pm = engine.DevicePlaneMap.empty(cam, (0.5, 16.0))
+        engine.random_init_device(pm, (0.5, 16.0), 3, "philox")
+        engine.run_patchmatch_device(prep, pm, 6, 3, workspace=ws, count_evals=True, check_valid=False,
+                                     skip_unchanged=skip)
+        out[skip] = (pm.depth.clone(), pm.normal.clone(), pm.cost.clone())
+        evals[skip] = int(ws.n_evals.item())
+    for a, b in zip(out[False], out[True]):
+        assert torch.equal(a, b)
+    assert evals[True] < evals[False], evals
+
+
+@pytest.mark.parametrize("precision", PRECISIONS)
 @pytest.mark.parametrize("n_views,top_k", [(4, 2), (4, 4), (6, 3), (3, 2), (1, 1)])
 def test_multi_view_topk_vs_oracle(pkg, oracle, n_views, top_k, precision):
     """V != 2 is unpinned by the reference; the oracle's per-view generalisation is the yardstick."""
