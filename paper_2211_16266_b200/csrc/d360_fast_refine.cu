@@ -7,6 +7,8 @@ namespace fast {
 
 // A CTA covers TW x TH_FULL pixels, one thread per pixel.  `flags` (optional, u8 per pixel):
 // set to 1 where a candidate was accepted, see d360_fast_rb.cu.
+__host__ __device__ inline size_t park_offset(size_t tile) { return (tile + 15) & ~(size_t)15; }
+
 template <class C>
 __global__ void __launch_bounds__(C::NT, C::MINB)
     k_refine(const __grid_constant__ FastGroup g, const __grid_constant__ RefineTable tab, float* __restrict__ depth,
@@ -15,6 +17,10 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
     extern __shared__ __align__(16) unsigned char smem[];
     const int x0 = blockIdx.x * TW, y0 = blockIdx.y * C::TH_FULL;
     const Tile t = tile_setup<C>(g, smem, x0, y0, C::TH_FULL, false, 0);
+    // loop-carried hypothesis (d, n) and cost of each thread, parked here while a candidate is
+    // evaluated: ten registers the evaluation's dependency chains can use instead
+    double* park = reinterpret_cast<double*>(smem + park_offset(tile_bytes(TW, C::TH_FULL, C::reach(g), false, C::V))) +
+                   threadIdx.x;
     __syncthreads();
     const int lx = threadIdx.x % TW, ly = threadIdx.x / TW;
     const int x = x0 + lx, y = y0 + ly;
@@ -23,14 +29,17 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
         const int R = C::reach(g);
         const int ce = (ly + R) * t.wwc + lx + R;
         const size_t i = (size_t)y * g.W + x;
-        double d = depth[i];
-        double nx = normal[3 * i], ny = normal[3 * i + 1], nz = normal[3 * i + 2];
-        double c = cost[i];
+        park[0 * C::NT] = depth[i];
+        park[1 * C::NT] = normal[3 * i];
+        park[2 * C::NT] = normal[3 * i + 1];
+        park[3 * C::NT] = normal[3 * i + 2];
+        park[4 * C::NT] = cost[i];
         double mr, sr;
         pixel_stats<C>(g, t, ce, mr, sr);
         bool accepted = false;
 #pragma unroll 1
         for (int k = 0; k < tab.n; ++k) {
+            const double d = park[0 * C::NT], nx = park[1 * C::NT], ny = park[2 * C::NT], nz = park[3 * C::NT];
             double nd = __dadd_rn(d, (double)tab.dd[k]);
             if (nd < tab.depth_min) nd = tab.depth_min;
             else if (nd > tab.depth_max) nd = tab.depth_max;
@@ -66,16 +75,17 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
             cnx = __dmul_rn(cnx, inv); cny = __dmul_rn(cny, inv); cnz = __dmul_rn(cnz, inv);
             const double ev = cand_cost<C, double>(g, t, ce, mr, sr, nd, cnx, cny, cnz);
             ++evals;
-            if (ev < c) {
-                c = ev; d = nd; nx = cnx; ny = cny; nz = cnz;
+            if (ev < park[4 * C::NT]) {
+                park[0 * C::NT] = nd; park[1 * C::NT] = cnx; park[2 * C::NT] = cny; park[3 * C::NT] = cnz;
+                park[4 * C::NT] = ev;
                 accepted = true;
             }
         }
-        depth[i] = (float)d;
-        normal[3 * i] = (float)nx;
-        normal[3 * i + 1] = (float)ny;
-        normal[3 * i + 2] = (float)nz;
-        cost[i] = (float)c;
+        depth[i] = (float)park[0 * C::NT];
+        normal[3 * i] = (float)park[1 * C::NT];
+        normal[3 * i + 1] = (float)park[2 * C::NT];
+        normal[3 * i + 2] = (float)park[3 * C::NT];
+        cost[i] = (float)park[4 * C::NT];
         if (flags != nullptr && accepted) flags[i] = 1;
     }
     if (n_evals != nullptr) {
@@ -93,7 +103,7 @@ int fast_refine(const GroupDev& gd, const RefineTable& tab, float* depth, float*
     FastGroup g;
     if (!make_fast_group(gd, &g)) return -1;
     D360_FAST_DISPATCH(gd.V, {
-        const size_t smem = tile_bytes(TW, C::TH_FULL, g.reach, false, gd.V);
+        const size_t smem = park_offset(tile_bytes(TW, C::TH_FULL, g.reach, false, gd.V)) + 5 * sizeof(double) * C::NT;
         if (smem > 200 * 1024) return -1;
         dim3 grid((gd.W + TW - 1) / TW, (gd.H + C::TH_FULL - 1) / C::TH_FULL);
         auto k = k_refine<C>;
