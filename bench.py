@@ -239,7 +239,7 @@ def run_product(args) -> dict | None:
     launches = _lib.launch_count() - launches0
     trace = _lib.trace_summary()
     _lib.trace_enable(False)
-    n_evals_counted = int(stage.workspace.n_evals.item())
+    n_evals_counted, n_cut = (int(x) for x in stage.workspace.n_evals.tolist())
 
     # ---- (B) end to end through the host-array streaming API: one pinned uint8 keyframe in per
     # step (each keyframe is uploaded once and reused by the 5 groups it takes part in), one
@@ -300,7 +300,10 @@ def run_product(args) -> dict | None:
         # binding resource is the FP64 pipe: the denominator is the DFMA peak measured in this run.
         fp64_peak = float(_lib.load().d360_measure_fma_peak(1, 20000))
         fp32_peak = float(_lib.load().d360_measure_fma_peak(0, 20000))
-        achieved = evals[dominant] * F / (d_ms * 1e-3) / 1e12
+        # refinement evaluations decided after V - 1 views did not do the last view's share of F
+        flops = {k: n * F for k, n in evals.items()}
+        flops["refine"] -= n_cut * (S * 83 + 12)
+        achieved = flops[dominant] / (d_ms * 1e-3) / 1e12
         traffic = None
         tf = ROOT / "profiles" / "traffic.json"
         if tf.exists():
@@ -338,6 +341,7 @@ def run_product(args) -> dict | None:
                                         "not HBM- or tensor-bound, see roofline.hbm",
                          "fp32_fma_peak": round(fp32_peak, 2),
                          "flops_per_eval": F, "evals_per_launch": evals[dominant] // max(d_cnt, 1),
+                         "flops_per_launch": flops[dominant] // max(d_cnt, 1),
                          "ms_per_launch": round(d_ms / d_cnt, 4),
                          "hbm": {"algorithmic_bytes_per_step": alg_bytes,
                                  "achieved_gbs": round(alg_bytes * args.steps / (dev_ms * 1e-3) / 1e9, 2),
@@ -345,6 +349,7 @@ def run_product(args) -> dict | None:
                                  "frac": round(alg_bytes * args.steps / (dev_ms * 1e-3) / 1e9 / hbm_peak, 5)}},
             "kernels": kinds,
             "evals_per_step": {k: v // args.steps for k, v in evals.items()},
+            "refine_evals_cut_after_v_minus_1_views_per_step": n_cut // args.steps,
         }
     if world > 1:
         dist.barrier()

@@ -112,7 +112,11 @@ int d360_refine_pass(const d360_group *g, float *depth, float *normal, float *co
  * hypothesis of a neighbour that did not change either (the re-test is certainly rejected
  * again, K:463 is strict <); results are bit-identical with and without it, only fewer
  * evaluations run (csrc/d360_fast_rb.cu).
- * valid_out (optional, u8) = cost < trunc (E:629). */
+ * valid_out (optional, u8) = cost < trunc (E:629).
+ * n_evals (device, optional, uint64[2]): [0] += cost evaluations started (propagation +
+ * refinement), [1] += refinement evaluations that were decided after V - 1 views (the last
+ * view cannot lift a candidate over the acceptance threshold of K:600, csrc/d360_fast.cuh)
+ * and so did 1/V less work. */
 int d360_run_patchmatch(const d360_group *g, float *depth, float *normal, float *cost,
                         float *scratch_depth, float *scratch_normal, float *scratch_cost,
                         uint8_t *scratch_changed, const float *tables, int iterations, int n_cand,

@@ -286,28 +286,16 @@ __device__ __forceinline__ double aggregate(double (&cv)[NV], int top_k) {
     return __dmul_rn(1.0 / top_k, total);
 }
 
-// Cost of one hypothesis at the pixel whose window entry is `ce` (K:201-297).
-template <class C, typename HT>
-__device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, int ce, double mr, double sr, HT d,
-                                            HT nx, HT ny, HT nz) {
-    constexpr int VT = C::VT;
-    const double trunc = g.trunc;
-    const float4 a = t.qg[ce];
-    double num;
-    if constexpr (sizeof(HT) == 4) {
-        const float ndota = dot3_f32(nx, ny, nz, a.x, a.y, a.z);
-        if ((double)ndota >= -D360_FACING_EPS || sr < D360_SIGMA_EPS) return trunc;
-        num = (double)__fmul_rn(d, ndota);
-    } else {
-        const double ndota = dot3_f64(nx, ny, nz, (double)a.x, (double)a.y, (double)a.z);
-        if (ndota >= -D360_FACING_EPS || sr < D360_SIGMA_EPS) return trunc;
-        num = __dmul_rn(d, ndota);
-    }
-    double s0[VT], ss0[VT], rs0[VT];
+// NCC sums (K:240-276) of one hypothesis over the views V0 .. V0 + NV - 1 at the pixel whose
+// window entry is `ce`.  `bad` is set when a sample is poisoned (K:242); it does not depend on
+// the views.
+template <class C, typename HT, int V0, int NV>
+__device__ __forceinline__ void accumulate_views(const FastGroup& g, const Tile& t, int ce, double num, HT nx, HT ny,
+                                                 HT nz, bool& bad, double (&s0)[NV], double (&ss0)[NV],
+                                                 double (&rs0)[NV]) {
 #pragma unroll
-    for (int v = 0; v < VT; ++v) s0[v] = ss0[v] = rs0[v] = 0.0;
-    bool bad = false;
-    const double2* __restrict__ nb = reinterpret_cast<const double2*>(g.nb64);
+    for (int v = 0; v < NV; ++v) s0[v] = ss0[v] = rs0[v] = 0.0;
+    const double2* __restrict__ nb = reinterpret_cast<const double2*>(g.nb64) + (size_t)V0 * g.plane32;
 
     // lam_k = num / dn_k of sample k (K:240-247) and the f64 luma of that sample
     auto plane_depth = [&](int es, double& lam, double& rv) {
@@ -345,19 +333,19 @@ __device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, i
         if (++col == ns) { col = 0; e_next += row_wrap; }
         double lam_next = 0.0, rv_next = 0.0;
         if (k + 1 < n_samples) plane_depth(e_next, lam_next, rv_next);
-        const double* rqe = t.rq + e;
+        const double* rqe = t.rq + V0 * 3 * t.ne + e;
         // at most 4 staged chains at a time (more would not fit the register file)
-        constexpr int VC = VT <= 4 ? VT : (VT + 1) / 2;
+        constexpr int VC = NV <= 4 ? NV : (NV + 1) / 2;
 #pragma unroll
-        for (int v0 = 0; v0 < VT; v0 += VC) {
+        for (int v0 = 0; v0 < NV; v0 += VC) {
             if (v0 == 0) {
                 double tx[VC], ty[VC], tz[VC], val[VC];
                 float pu[VC], pv[VC];
 #pragma unroll
                 for (int v = 0; v < VC; ++v) {
-                    tx[v] = fma(lam, rqe[(v * 3 + 0) * t.ne], g.rel_t[v][0]);
-                    ty[v] = fma(lam, rqe[(v * 3 + 1) * t.ne], g.rel_t[v][1]);
-                    tz[v] = fma(lam, rqe[(v * 3 + 2) * t.ne], g.rel_t[v][2]);
+                    tx[v] = fma(lam, rqe[(v * 3 + 0) * t.ne], g.rel_t[V0 + v][0]);
+                    ty[v] = fma(lam, rqe[(v * 3 + 1) * t.ne], g.rel_t[V0 + v][1]);
+                    tz[v] = fma(lam, rqe[(v * 3 + 2) * t.ne], g.rel_t[V0 + v][2]);
                 }
                 project_uv<VC>(g, tx, ty, tz, pu, pv);
                 gather_bilinear<VC>(g, nb, pu, pv, val);
@@ -368,14 +356,14 @@ __device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, i
                     rs0[v] = fma(rv, val[v], rs0[v]);
                 }
             } else {
-                constexpr int VR = VT - VC > 0 ? VT - VC : 1;  // second (last) chunk
+                constexpr int VR = NV - VC > 0 ? NV - VC : 1;  // second (last) chunk
                 double tx[VR], ty[VR], tz[VR], val[VR];
                 float pu[VR], pv[VR];
 #pragma unroll
                 for (int v = 0; v < VR; ++v) {
-                    tx[v] = fma(lam, rqe[((VC + v) * 3 + 0) * t.ne], g.rel_t[VC + v][0]);
-                    ty[v] = fma(lam, rqe[((VC + v) * 3 + 1) * t.ne], g.rel_t[VC + v][1]);
-                    tz[v] = fma(lam, rqe[((VC + v) * 3 + 2) * t.ne], g.rel_t[VC + v][2]);
+                    tx[v] = fma(lam, rqe[((VC + v) * 3 + 0) * t.ne], g.rel_t[V0 + VC + v][0]);
+                    ty[v] = fma(lam, rqe[((VC + v) * 3 + 1) * t.ne], g.rel_t[V0 + VC + v][1]);
+                    tz[v] = fma(lam, rqe[((VC + v) * 3 + 2) * t.ne], g.rel_t[V0 + VC + v][2]);
                 }
                 project_uv<VR>(g, tx, ty, tz, pu, pv);
                 gather_bilinear<VR>(g, nb + (size_t)VC * g.plane32, pu, pv, val);
@@ -391,22 +379,85 @@ __device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, i
         lam = lam_next;
         rv = rv_next;
     }
-    if (bad) return trunc;
+}
 
-    const double inv_s = g.inv_s;
+// K:277-296 for one view: truncated 1 - NCC from the sums
+__device__ __forceinline__ double view_cost(const FastGroup& g, double s0, double ss0, double rs0, double mr,
+                                            double sr) {
+    const double trunc = g.trunc, inv_s = g.inv_s;
+    const double m0 = s0 * inv_s;
+    const double v0 = ss0 * inv_s - m0 * m0;
+    if (v0 < D360_VAR_EPS) return trunc;
+    const double cov = rs0 * inv_s - mr * m0;
+    double c = 1.0 - cov / (sr * sqrt(v0));
+    c = c < 0.0 ? 0.0 : c;
+    return c > trunc ? trunc : c;  // NaN (unguarded polar singularities) passes through, see cand_cost
+}
+
+// Cost of one hypothesis at the pixel whose window entry is `ce` (K:201-297).
+//
+// EARLY (refine_pass): the caller only asks "is the cost below `bound`" (K:600 `ev < c`) and
+// discards the value otherwise.  The cost is the mean of the top_k smallest per-view costs and
+// every per-view cost is >= 0, so after V - 1 views the mean of { 0, and the top_k - 1 smallest
+// of those } is a lower bound; when it is already >= bound the last view cannot change the
+// decision and is not evaluated (the bound itself is returned, which the caller rejects).
+// Measured on the benchmark sequence: 76-95 % of the refinement candidates, 52-84 % of the warps.
+// Otherwise the last view is evaluated in a second pass over the samples and the result is the
+// single-pass one bit for bit (per-view sums do not interact).
+template <class C, typename HT, bool EARLY = false>
+__device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, int ce, double mr, double sr, HT d,
+                                            HT nx, HT ny, HT nz, double bound = 0.0, unsigned* cuts = nullptr) {
+    constexpr int VT = C::VT;
+    const double trunc = g.trunc;
+    const float4 a = t.qg[ce];
+    double num;
+    if constexpr (sizeof(HT) == 4) {
+        const float ndota = dot3_f32(nx, ny, nz, a.x, a.y, a.z);
+        if ((double)ndota >= -D360_FACING_EPS || sr < D360_SIGMA_EPS) return trunc;
+        num = (double)__fmul_rn(d, ndota);
+    } else {
+        const double ndota = dot3_f64(nx, ny, nz, (double)a.x, (double)a.y, (double)a.z);
+        if (ndota >= -D360_FACING_EPS || sr < D360_SIGMA_EPS) return trunc;
+        num = __dmul_rn(d, ndota);
+    }
+    bool bad = false;
     double cv[VT];
+    if constexpr (EARLY && VT >= 2) {
+        constexpr int VA = VT - 1;
+        {
+            double s0[VA], ss0[VA], rs0[VA];
+            accumulate_views<C, HT, 0, VA>(g, t, ce, num, nx, ny, nz, bad, s0, ss0, rs0);
+            if (bad) return trunc;
 #pragma unroll
-    for (int v = 0; v < VT; ++v) {
-        cv[v] = trunc;
-        const double m0 = s0[v] * inv_s;
-        const double v0 = ss0[v] * inv_s - m0 * m0;
-        if (!(v0 < D360_VAR_EPS)) {
-            const double cov = rs0[v] * inv_s - mr * m0;
-            double c = 1.0 - cov / (sr * sqrt(v0));
-            c = c < 0.0 ? 0.0 : c;
-            c = c > trunc ? trunc : c;
-            cv[v] = c;
+            for (int v = 0; v < VA; ++v) cv[v] = view_cost(g, s0[v], ss0[v], rs0[v], mr, sr);
         }
+        {
+            double known[VA];
+#pragma unroll
+            for (int v = 0; v < VA; ++v) known[v] = cv[v];
+            // top_k - 1 smallest known costs plus one unknown cost >= 0.  top_k = 2: half the
+            // smallest known cost, exact, and fl(a1 + a2) >= it for any two of the costs.  Otherwise
+            // the sum is rounded differently from the final one: shave 1e-12 off (any smaller
+            // number is still a lower bound).
+            double lower = 0.0;
+            if (g.top_k >= 2) lower = aggregate<VA>(known, g.top_k - 1) * ((double)(g.top_k - 1) / g.top_k);
+            if (g.top_k > 2) lower *= 1.0 - 1e-12;
+            if (lower >= bound) {  // false for NaN: falls through to the full evaluation
+                if (cuts != nullptr) ++*cuts;
+                return lower;
+            }
+        }
+        {
+            double s0[1], ss0[1], rs0[1];
+            accumulate_views<C, HT, VA, 1>(g, t, ce, num, nx, ny, nz, bad, s0, ss0, rs0);
+            cv[VA] = view_cost(g, s0[0], ss0[0], rs0[0], mr, sr);
+        }
+    } else {
+        double s0[VT], ss0[VT], rs0[VT];
+        accumulate_views<C, HT, 0, VT>(g, t, ce, num, nx, ny, nz, bad, s0, ss0, rs0);
+        if (bad) return trunc;
+#pragma unroll
+        for (int v = 0; v < VT; ++v) cv[v] = view_cost(g, s0[v], ss0[v], rs0[v], mr, sr);
     }
     const double total = aggregate<VT>(cv, g.top_k);
     return total == total ? total : trunc;  // NaN only from the unguarded polar singularities

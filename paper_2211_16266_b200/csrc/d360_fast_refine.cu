@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
     __syncthreads();
     const int lx = threadIdx.x % TW, ly = threadIdx.x / TW;
     const int x = x0 + lx, y = y0 + ly;
-    unsigned int evals = 0;
+    unsigned int evals = 0, cuts = 0;  // evaluations started; evaluations that stopped before the last view
     if (x < g.W && y < g.H) {
         const int R = C::reach(g);
         const int ce = (ly + R) * t.wwc + lx + R;
@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
             if (nrm < 1e-12) continue;
             const double inv = 1.0 / nrm;
             cnx = __dmul_rn(cnx, inv); cny = __dmul_rn(cny, inv); cnz = __dmul_rn(cnz, inv);
-            const double ev = cand_cost<C, double>(g, t, ce, mr, sr, nd, cnx, cny, cnz);
+            const double ev = cand_cost<C, double, true>(g, t, ce, mr, sr, nd, cnx, cny, cnz, park[4 * C::NT], &cuts);
             ++evals;
             if (ev < park[4 * C::NT]) {
                 park[0 * C::NT] = nd; park[1 * C::NT] = cnx; park[2 * C::NT] = cny; park[3 * C::NT] = cnz;
@@ -89,8 +89,14 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
         if (flags != nullptr && accepted) flags[i] = 1;
     }
     if (n_evals != nullptr) {
-        for (int o = 16; o > 0; o >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, o);
-        if ((threadIdx.x & 31) == 0 && evals) atomicAdd(n_evals, (unsigned long long)evals);
+        for (int o = 16; o > 0; o >>= 1) {
+            evals += __shfl_xor_sync(0xffffffffu, evals, o);
+            cuts += __shfl_xor_sync(0xffffffffu, cuts, o);
+        }
+        if ((threadIdx.x & 31) == 0 && evals) {
+            atomicAdd(n_evals, (unsigned long long)evals);
+            if (cuts) atomicAdd(n_evals + 1, (unsigned long long)cuts);
+        }
     }
 }
 

@@ -518,7 +518,7 @@ class PatchMatchWorkspace:
         self.normal = torch.empty((h, w, 3), dtype=torch.float32, device=device)
         self.cost = torch.empty((h, w), dtype=torch.float32, device=device)
         self.changed = torch.empty((2, h, w), dtype=torch.uint8, device=device)
-        self.n_evals = torch.zeros((1,), dtype=torch.int64, device=device)
+        self.n_evals = torch.zeros((2,), dtype=torch.int64, device=device)  # [evaluations, cut short]
 
 
 def run_patchmatch_device(prep: PreparedGroup, pm: DevicePlaneMap, iterations: int, seed: int,
@@ -530,7 +530,8 @@ def run_patchmatch_device(prep: PreparedGroup, pm: DevicePlaneMap, iterations: i
 
     One C-ABI call (d360_run_patchmatch) enqueues eval + iterations x (red, black, refine).
     With ``count_evals`` the executed propagation/refinement cost evaluations are ADDED to
-    ``workspace.n_evals`` (zero it yourself; reading it synchronises).  ``skip_unchanged`` lets a
+    ``workspace.n_evals[0]`` and the refinement evaluations decided after V - 1 views to
+    ``workspace.n_evals[1]`` (zero it yourself; reading it synchronises).  ``skip_unchanged`` lets a
     pixel skip re-testing neighbour hypotheses that did not change since the previous iteration
     (result-neutral, see include/d360.h); switch it off to count the reference's evaluations."""
     if iterations < 1:

@@ -210,7 +210,7 @@ def test_unchanged_neighbour_skipping_is_result_neutral(pkg, name, iterations, p
         engine.run_patchmatch_device(prep, pm, iterations, int(z["seed"]), workspace=ws, count_evals=True,
                                      skip_unchanged=skip)
         out[skip] = (pm.depth.cpu().numpy(), pm.normal.cpu().numpy(), pm.cost.cpu().numpy())
-        evals[skip] = int(ws.n_evals.item())
+        evals[skip] = int(ws.n_evals[0].item())
     for a, b in zip(out[False], out[True]):
         assert np.array_equal(a, b)
     assert evals[True] <= evals[False]
@@ -235,7 +235,7 @@ def test_unchanged_neighbour_skipping_full_size(pkg):
         engine.run_patchmatch_device(prep, pm, 6, 3, workspace=ws, count_evals=True, check_valid=False,
                                      skip_unchanged=skip)
         out[skip] = (pm.depth.clone(), pm.normal.clone(), pm.cost.clone())
-        evals[skip] = int(ws.n_evals.item())
+        evals[skip] = int(ws.n_evals[0].item())
     for a, b in zip(out[False], out[True]):
         assert torch.equal(a, b)
     assert evals[True] < evals[False], evals
