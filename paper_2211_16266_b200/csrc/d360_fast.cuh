@@ -37,6 +37,9 @@ constexpr int TW = 32;  // tile width (pixels)
 #ifndef D360_MINB
 #define D360_MINB 2  // CTAs per SM the register budget is sized for (128 registers)
 #endif
+#ifndef D360_VC_MAX
+#define D360_VC_MAX 4  // views whose projection chains are staged side by side
+#endif
 
 struct FastGroup {
     int W, H, ns, stride, reach, top_k;
@@ -335,7 +338,7 @@ __device__ __forceinline__ void accumulate_views(const FastGroup& g, const Tile&
         if (k + 1 < n_samples) plane_depth(e_next, lam_next, rv_next);
         const double* rqe = t.rq + V0 * 3 * t.ne + e;
         // at most 4 staged chains at a time (more would not fit the register file)
-        constexpr int VC = NV <= 4 ? NV : (NV + 1) / 2;
+        constexpr int VC = NV <= D360_VC_MAX ? NV : (NV + 1) / 2;
 #pragma unroll
         for (int v0 = 0; v0 < NV; v0 += VC) {
             if (v0 == 0) {

@@ -29,4 +29,4 @@ for name in sys.argv[1:] or list(CONFIGS):
     tot = sum(ms for _, ms in tr.values())
     print(name, f"{W}x{H} V={V} S={len(prep.offsets)} I={it}: total {tot:.2f} ms",
           {k: round(ms / n, 3) for k, (n, ms) in tr.items() if k in ("red_black", "refine", "eval_costs")},
-          "evals", int(ws.n_evals.item()), f"within2pct&valid {ok:.3f}", flush=True)
+          "evals", ws.n_evals.tolist(), f"within2pct&valid {ok:.3f}", flush=True)

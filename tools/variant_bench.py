@@ -24,4 +24,4 @@ ok = ((pm.depth - gt_t).abs() / gt_t < 0.02).float().mean().item()
 tot = sum(ms for _, ms in tr.values())
 print(os.environ.get("D360_LIB_PATH", "default"), "total ms %.2f" % tot,
       {k: round(ms / n, 3) for k, (n, ms) in tr.items() if k in ("red_black", "refine", "eval_costs")},
-      "evals", int(ws.n_evals.item()), "within2pct %.4f" % ok, "cost sum %.6f" % pm.cost.double().sum().item())
+      "evals", ws.n_evals.tolist(), "within2pct %.4f" % ok, "cost sum %.6f" % pm.cost.double().sum().item())
