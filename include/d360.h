@@ -203,6 +203,41 @@ int d360_render_box_scene(const double *size_xyz, int texture_seed, double noise
  * fp64 != 0 measures the DFMA pipe instead.  Synchronous. */
 double d360_measure_fma_peak(int fp64, int iters);
 
+/* ---- output packing and metrics --------------------- */
+
+/* replaces the record packing of outputs.write_ply (outputs.py:30-54): n records of 15 bytes,
+ * (x, y, z) = astype(float32) of the f64 world points, little endian, then r, g, b. */
+int d360_pack_ply_records(const double *points, const uint8_t *colors, uint8_t *records,
+                          int64_t n, void *stream);
+
+/* replaces the quantisation of outputs.write_depth_png (outputs.py:81-97):
+ * mm = clip(rint(depth * 1000), 0, 65535) in f64 as u16, 0 where invalid.  stats (device,
+ * 3 x uint32, written): valid count, and the min / max valid depth as order-preserving keys
+ * (key = bits ^ (sign ? 0xffffffff : 0x80000000)) for the JSON sidecar. */
+int d360_depth_to_mm16(const float *depth, const uint8_t *valid, uint16_t *mm, uint32_t *stats,
+                       int height, int width, void *stream);
+
+/* replaces the per-pose splat of metrics.completeness (metrics.py:31-45): marks
+ * raster[py, px] = 1 (u8 (height, width), zeroed by the caller) for every point. */
+int d360_completeness_splat(const double *points, int64_t n, const double *rot,
+                            const double *trans, uint8_t *raster, int height, int width,
+                            void *stream);
+/* *count (device) += number of nonzero bytes */
+int d360_count_nonzero(const uint8_t *a, int64_t n, unsigned long long *count, void *stream);
+
+/* replaces metrics.accuracy (metrics.py:52-78): out (device, 4 doubles) = { sum |p-g|/g,
+ * sum (p-g)^2, #(|p-g|/g <= 0.02), #jointly valid }; scratch: device,
+ * d360_accuracy_scratch_doubles() doubles.  Fixed reduction order (run-to-run identical). */
+int d360_accuracy_scratch_doubles(void);
+int d360_depth_accuracy(const float *pred_depth, const uint8_t *pred_valid, const float *gt_depth,
+                        const uint8_t *gt_valid, int64_t n, double *scratch, double *out,
+                        void *stream);
+
+/* metrics.voxel_occupancy (metrics.py:81-87): keys[i] = floor(p / voxel) per axis packed
+ * 3 x 21 bits; *overflow (device int) set if a cell index leaves [-2^20, 2^20). */
+int d360_voxel_keys(const double *points, int64_t n, double voxel, long long *keys, int *overflow,
+                    void *stream);
+
 #ifdef __cplusplus
 }
 #endif

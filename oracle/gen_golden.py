@@ -199,7 +199,56 @@ def misc_case():
     print("misc ok")
 
 
+def io_metrics_case():
+    """Output writers (outputs.py) and metrics (metrics.py): bytes / numbers of the reference."""
+    import tempfile
+
+    from densify360 import metrics, outputs
+    from densify360.pipeline import FusedCloud
+
+    rng = np.random.default_rng(31)
+    n = 257
+    pts = rng.normal(size=(n, 3)) * np.array([2.0, 1.0, 3.0]) + np.array([0.1, -0.2, 0.3])
+    pts[5] = (0.1, -0.2, 0.3)  # coincides with the first pose centre: dropped by completeness (r <= 1e-12)
+    cols = rng.integers(0, 256, size=(n, 3), dtype=np.uint8)
+    cloud = FusedCloud(pts, cols, np.zeros(n, np.int64))
+    cam = EquirectCamera(32, 16)
+    depth = rng.uniform(0.2, 70.0, size=(16, 32)).astype(np.float32)  # > 65.535 m clips
+    depth[2, 3] = 1.0005  # rint half-to-even candidates in millimetres
+    depth[2, 4] = 2.0015
+    valid = rng.uniform(size=(16, 32)) > 0.25
+    pano = engine.DepthPanorama(cam, depth, valid)
+    with tempfile.TemporaryDirectory() as d:
+        outputs.write_ply(Path(d) / "c.ply", cloud)
+        ply = np.frombuffer((Path(d) / "c.ply").read_bytes(), np.uint8)
+        outputs.write_depth_png(Path(d) / "d.png", pano)
+        png = np.frombuffer((Path(d) / "d.png").read_bytes(), np.uint8)
+        sidecar = (Path(d) / "d.json").read_text()
+        back = outputs.read_depth_png(Path(d) / "d.png")
+    poses = [RigidPose(np.eye(3), np.array([0.1, -0.2, 0.3])),
+             RigidPose(rot(1, 33.0) @ rot(0, -12.0), np.array([-0.5, 0.1, 0.9])),
+             RigidPose(rot(2, 80.0), np.array([1.5, 0.4, -2.0]))]
+    comp_cam = EquirectCamera(72, 36)
+    comp = metrics.completeness(pts, poses, comp_cam)
+    comp_default = metrics.completeness(pts, poses[:2])
+    gt = engine.DepthPanorama(cam, (depth * rng.uniform(0.97, 1.03, size=depth.shape)).astype(np.float32),
+                              rng.uniform(size=(16, 32)) > 0.2)
+    acc = metrics.accuracy(pano, gt)
+    vox = [metrics.voxel_occupancy(pts, v) for v in (0.1, 0.5, 2.0)]
+    np.savez_compressed(OUT / "io_metrics.npz", points=pts, colors=cols, ply=ply, depth=depth, valid=valid, png=png,
+                        sidecar=np.array(sidecar), back_depth=back.depth, back_valid=back.valid,
+                        pose_r=np.stack([p.rotation for p in poses]), pose_t=np.stack([p.translation for p in poses]),
+                        comp_series=np.array(comp["per_keyframe"]), comp_mean=comp["mean"],
+                        comp_default_series=np.array(comp_default["per_keyframe"]), gt_depth=gt.depth,
+                        gt_valid=gt.valid, acc=np.array([acc["mean_abs_rel"], acc["rmse_m"], acc["inlier_2pc"],
+                                                          acc["valid_pixels"]]), vox=np.array(vox))
+    print("io/metrics ok", len(ply), len(png), comp["per_keyframe"], acc, vox)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["io"]:
+        io_metrics_case()
+        sys.exit(0)
     ident = lambda z: RigidPose(rotation=np.eye(3), translation=np.array([0.0, 0.0, z]))
     hot_path_case("hot_64x32_ident", 64, 3, [ident(-0.15), ident(0.0), ident(0.15)], PatchSpec(), 7, True)
     rposes = [RigidPose(rot(1, -7.0) @ rot(0, 3.0), np.array([0.05, -0.02, -0.17])),
@@ -209,3 +258,4 @@ if __name__ == "__main__":
     hot_path_case("hot_256x128_c1", 256, 3, [ident(-0.15), ident(0.0), ident(0.15)], PatchSpec(), 0, False)
     stage_case()
     misc_case()
+    io_metrics_case()

@@ -10,7 +10,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libd360.so"
 SOURCES = ["d360_common.cu", "d360_aux.cu", "d360_patchmatch.cu", "d360_fast.cu", "d360_fast_eval.cu",
-           "d360_fast_rb.cu", "d360_fast_refine.cu"]
+           "d360_fast_rb.cu", "d360_fast_refine.cu", "d360_io.cu"]
 HEADERS = [CSRC / "d360_device.cuh", CSRC / "d360_fast.cuh", PKG.parent / "include" / "d360.h"]
 NVCC_FLAGS = ["-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
               "-Xcompiler", "-fPIC"]

@@ -68,6 +68,13 @@ _SIGNATURES = {
     "d360_render_box_scene": (C.c_int, [c_void, C.c_int, C.c_double, C.c_int, c_void, c_void, c_void, c_void,
                                         c_void, C.c_int, C.c_int, c_void]),
     "d360_measure_fma_peak": (C.c_double, [C.c_int, C.c_int]),
+    "d360_pack_ply_records": (C.c_int, [c_void, c_void, c_void, C.c_int64, c_void]),
+    "d360_depth_to_mm16": (C.c_int, [c_void, c_void, c_void, c_void, C.c_int, C.c_int, c_void]),
+    "d360_completeness_splat": (C.c_int, [c_void, C.c_int64, c_void, c_void, c_void, C.c_int, C.c_int, c_void]),
+    "d360_count_nonzero": (C.c_int, [c_void, C.c_int64, c_void, c_void]),
+    "d360_accuracy_scratch_doubles": (C.c_int, []),
+    "d360_depth_accuracy": (C.c_int, [c_void, c_void, c_void, c_void, C.c_int64, c_void, c_void, c_void]),
+    "d360_voxel_keys": (C.c_int, [c_void, C.c_int64, C.c_double, c_void, c_void, c_void]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)

@@ -597,3 +597,65 @@ def test_run_patchmatch_end_to_end_v4_topk_vs_oracle(pkg, oracle):
     same = (pm.depth == od) & (pm.normal == on).all(-1)
     assert same.mean() >= 0.99  # in fact the trajectories stay identical almost everywhere
     assert cost_close(pm.cost[same], oc[same]).all()
+
+
+def test_output_writers_match_reference_bytes(pkg, tmp_path):
+    """f3: the PLY and depth-PNG bytes (and the JSON sidecar) equal the reference's writers'."""
+    p, engine, pipeline, _ = pkg
+    from paper_2211_16266_b200 import outputs
+
+    z = load_golden("io_metrics")
+    cloud = pipeline.FusedCloud(z["points"], z["colors"], np.zeros(len(z["points"]), np.int64))
+    outputs.write_ply(tmp_path / "c.ply", cloud)
+    assert (tmp_path / "c.ply").read_bytes() == z["ply"].tobytes()
+    # device batches (what the streaming pipeline produces), split in two
+    dev = torch.device("cuda")
+    pts, cols = torch.from_numpy(z["points"]).to(dev), torch.from_numpy(z["colors"]).to(dev)
+    batches = [pipeline.DeviceFusedCloud(pts[:100], cols[:100], 0), pipeline.DeviceFusedCloud(pts[100:], cols[100:], 1)]
+    outputs.write_ply(tmp_path / "d.ply", batches)
+    assert (tmp_path / "d.ply").read_bytes() == z["ply"].tobytes()
+    back_p, back_c = outputs.read_ply(tmp_path / "c.ply")
+    assert np.array_equal(back_p, z["points"].astype(np.float32).astype(np.float64)) and np.array_equal(back_c, z["colors"])
+    outputs.write_ply(tmp_path / "e.ply", pipeline.FusedCloud.empty())
+    assert outputs.read_ply(tmp_path / "e.ply")[0].shape == (0, 3)
+
+    cam = p.EquirectCamera(32, 16)
+    pano = engine.DepthPanorama(cam, z["depth"], z["valid"])
+    outputs.write_depth_png(tmp_path / "d.png", pano)
+    assert (tmp_path / "d.png").read_bytes() == z["png"].tobytes()
+    assert (tmp_path / "d.json").read_text() == str(z["sidecar"])
+    back = outputs.read_depth_png(tmp_path / "d.png")
+    assert np.array_equal(back.depth, z["back_depth"]) and np.array_equal(back.valid, z["back_valid"])
+    none = engine.DepthPanorama(cam, z["depth"], np.zeros_like(z["valid"]))
+    outputs.write_depth_png(tmp_path / "n.png", none)
+    assert '"valid_count": 0' in (tmp_path / "n.json").read_text() and '"depth_min_m": null' in (tmp_path / "n.json").read_text()
+
+
+def test_metrics_match_reference(pkg):
+    """f4: completeness rasters exact (counts are integers), accuracy sums to 1e-12, voxels exact."""
+    p, engine, _, _ = pkg
+    from paper_2211_16266_b200 import metrics
+
+    z = load_golden("io_metrics")
+    poses = [p.RigidPose(r, t) for r, t in zip(z["pose_r"], z["pose_t"])]
+    comp = metrics.completeness(z["points"], poses, p.EquirectCamera(72, 36))
+    assert comp["per_keyframe"] == z["comp_series"].tolist() and comp["mean"] == float(z["comp_mean"])
+    assert comp["point_count"] == len(z["points"]) and comp["resolution"] == [72, 36]
+    assert metrics.completeness(z["points"], poses[:2])["per_keyframe"] == z["comp_default_series"].tolist()
+    assert metrics.completeness(np.zeros((0, 3)), poses)["per_keyframe"] == [0.0, 0.0, 0.0]
+    assert metrics.completeness(z["points"], [])["mean"] == 0.0
+    cam = p.EquirectCamera(32, 16)
+    pred, gt = engine.DepthPanorama(cam, z["depth"], z["valid"]), engine.DepthPanorama(cam, z["gt_depth"], z["gt_valid"])
+    acc = metrics.accuracy(pred, gt)
+    want = z["acc"]
+    assert acc["valid_pixels"] == int(want[3]) and acc["defined"]
+    assert abs(acc["mean_abs_rel"] - want[0]) <= 1e-12 * want[0] and abs(acc["rmse_m"] - want[1]) <= 1e-12 * want[1]
+    assert acc["inlier_2pc"] == want[2]
+    assert metrics.accuracy(pred, gt) == acc  # fixed reduction order
+    empty = metrics.accuracy(pred, engine.DepthPanorama(cam, z["gt_depth"], np.zeros_like(z["gt_valid"])))
+    assert not empty["defined"] and empty["valid_pixels"] == 0 and np.isnan(empty["rmse_m"])
+    with pytest.raises(ValueError):
+        metrics.accuracy(pred, engine.DepthPanorama(p.EquirectCamera(64, 32), np.ones((32, 64), np.float32),
+                                                    np.ones((32, 64), bool)))
+    assert [metrics.voxel_occupancy(z["points"], v) for v in (0.1, 0.5, 2.0)] == z["vox"].tolist()
+    assert metrics.voxel_occupancy(np.zeros((0, 3))) == 0
