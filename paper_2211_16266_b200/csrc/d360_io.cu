@@ -12,23 +12,36 @@ namespace d360 {
 static inline unsigned io_blocks(size_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
 
 // O:30-54: record = astype(float32) of (x, y, z), little endian, then r, g, b (15 bytes, packed).
-// One thread per record; the 15 byte stores of a warp cover 480 contiguous bytes.
-__global__ void k_pack_ply(const double* __restrict__ pts, const uint8_t* __restrict__ rgb, uint8_t* __restrict__ rec,
-                           size_t n) {
-    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    uint8_t* o = rec + 15 * i;
+// A block packs 256 records into shared memory and writes them out as 240 aligned 16-byte
+// stores (a record-per-thread byte store pattern runs at a sixth of the HBM rate).
+constexpr int PLY_BLOCK = 256;
+__global__ void __launch_bounds__(PLY_BLOCK)
+    k_pack_ply(const double* __restrict__ pts, const uint8_t* __restrict__ rgb, uint8_t* __restrict__ rec, size_t n) {
+    __shared__ __align__(16) uint8_t sh[PLY_BLOCK * 15];
+    const size_t base = (size_t)blockIdx.x * PLY_BLOCK;
+    const size_t i = base + threadIdx.x;
+    if (i < n) {
+        uint8_t* o = sh + 15 * threadIdx.x;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        const unsigned b = __float_as_uint(__double2float_rn(pts[3 * i + c]));
-        o[4 * c + 0] = (uint8_t)(b);
-        o[4 * c + 1] = (uint8_t)(b >> 8);
-        o[4 * c + 2] = (uint8_t)(b >> 16);
-        o[4 * c + 3] = (uint8_t)(b >> 24);
+        for (int c = 0; c < 3; ++c) {
+            const unsigned b = __float_as_uint(__double2float_rn(pts[3 * i + c]));
+            o[4 * c + 0] = (uint8_t)(b);
+            o[4 * c + 1] = (uint8_t)(b >> 8);
+            o[4 * c + 2] = (uint8_t)(b >> 16);
+            o[4 * c + 3] = (uint8_t)(b >> 24);
+        }
+        o[12] = rgb[3 * i];
+        o[13] = rgb[3 * i + 1];
+        o[14] = rgb[3 * i + 2];
     }
-    o[12] = rgb[3 * i];
-    o[13] = rgb[3 * i + 1];
-    o[14] = rgb[3 * i + 2];
+    __syncthreads();
+    const size_t n_here = n - base < (size_t)PLY_BLOCK ? n - base : (size_t)PLY_BLOCK;
+    const size_t bytes = n_here * 15;
+    uint8_t* out = rec + base * 15;  // 3840 * blockIdx: 16-byte aligned when rec is
+    const size_t vec = ((reinterpret_cast<uintptr_t>(out) & 15) == 0) ? bytes / 16 : 0;
+    for (size_t k = threadIdx.x; k < vec; k += PLY_BLOCK)
+        reinterpret_cast<uint4*>(out)[k] = reinterpret_cast<const uint4*>(sh)[k];
+    for (size_t k = vec * 16 + threadIdx.x; k < bytes; k += PLY_BLOCK) out[k] = sh[k];
 }
 
 // order-preserving map f32 -> u32 (for atomicMin / atomicMax on depths of any sign)
@@ -44,20 +57,24 @@ __global__ void k_mm16_init(unsigned* stats) {
 }
 
 // O:81-97: mm = clip(rint(depth * 1000), 0, 65535) computed in f64, 0 where invalid; the sidecar's
-// valid count and min / max valid depth come out of the same pass.
-__global__ void k_depth_to_mm16(const float* __restrict__ depth, const uint8_t* __restrict__ valid,
-                                uint16_t* __restrict__ mm, unsigned* stats, size_t n) {
-    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+// valid count and min / max valid depth come out of the same pass (grid-stride, one set of
+// atomics per block).
+constexpr int MM_THREADS = 256;
+__global__ void __launch_bounds__(MM_THREADS)
+    k_depth_to_mm16(const float* __restrict__ depth, const uint8_t* __restrict__ valid, uint16_t* __restrict__ mm,
+                    unsigned* stats, size_t n) {
     unsigned cnt = 0, kmin = 0xffffffffu, kmax = 0u;
-    if (i < n) {
+    for (size_t i = (size_t)blockIdx.x * MM_THREADS + threadIdx.x; i < n; i += (size_t)gridDim.x * MM_THREADS) {
         const float d = depth[i];
         double v = rint((double)d * 1000.0);  // np.rint: half to even
         v = v < 0.0 ? 0.0 : (v > 65535.0 ? 65535.0 : v);
         const bool ok = valid[i] != 0;
         mm[i] = ok ? (uint16_t)v : (uint16_t)0;
         if (ok) {
-            cnt = 1;
-            kmin = kmax = f32_key(d);
+            const unsigned k = f32_key(d);
+            ++cnt;
+            kmin = min(kmin, k);
+            kmax = max(kmax, k);
         }
     }
     for (int o = 16; o > 0; o >>= 1) {
@@ -65,10 +82,24 @@ __global__ void k_depth_to_mm16(const float* __restrict__ depth, const uint8_t* 
         kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
         kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
     }
-    if ((threadIdx.x & 31) == 0 && cnt) {
-        atomicAdd(&stats[0], cnt);
-        atomicMin(&stats[1], kmin);
-        atomicMax(&stats[2], kmax);
+    __shared__ unsigned sh[3][MM_THREADS / 32];
+    if ((threadIdx.x & 31) == 0) {
+        sh[0][threadIdx.x >> 5] = cnt;
+        sh[1][threadIdx.x >> 5] = kmin;
+        sh[2][threadIdx.x >> 5] = kmax;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < MM_THREADS / 32; ++w) {
+            cnt += sh[0][w];
+            kmin = min(kmin, sh[1][w]);
+            kmax = max(kmax, sh[2][w]);
+        }
+        if (cnt) {
+            atomicAdd(&stats[0], cnt);
+            atomicMin(&stats[1], kmin);
+            atomicMax(&stats[2], kmax);
+        }
     }
 }
 
@@ -112,7 +143,7 @@ __global__ void k_count_nonzero(const uint8_t* __restrict__ a, size_t n, unsigne
 
 // M:52-78 over jointly valid pixels: sum |p - g| / g, sum (p - g)^2, #(rel <= 0.02), #joint.
 // Two stages with a fixed reduction order, so the f64 sums are the same on every run.
-constexpr int ACC_BLOCKS = 256, ACC_THREADS = 256;
+constexpr int ACC_BLOCKS = 1024, ACC_THREADS = 256;
 __global__ void __launch_bounds__(ACC_THREADS)
     k_accuracy_partial(const float* __restrict__ pd, const uint8_t* __restrict__ pv, const float* __restrict__ gd,
                        const uint8_t* __restrict__ gv, size_t n, double* __restrict__ partial) {
@@ -177,7 +208,7 @@ extern "C" int d360_pack_ply_records(const double* points, const uint8_t* colors
     if (n == 0) return 0;
     {
         TraceScope ts_("pack_ply", (cudaStream_t)stream);
-        k_pack_ply<<<io_blocks((size_t)n, 256), 256, 0, (cudaStream_t)stream>>>(points, colors, records, (size_t)n);
+        k_pack_ply<<<io_blocks((size_t)n, PLY_BLOCK), PLY_BLOCK, 0, (cudaStream_t)stream>>>(points, colors, records, (size_t)n);
     }
     return check_launch("pack_ply_records");
 }
@@ -188,7 +219,7 @@ extern "C" int d360_depth_to_mm16(const float* depth, const uint8_t* valid, uint
     {
         TraceScope ts_("depth_to_mm16", (cudaStream_t)stream);
         k_mm16_init<<<1, 1, 0, (cudaStream_t)stream>>>(stats);
-        k_depth_to_mm16<<<io_blocks(n, 256), 256, 0, (cudaStream_t)stream>>>(depth, valid, mm, stats, n);
+        k_depth_to_mm16<<<min(io_blocks(n, MM_THREADS), 148u * 8u), MM_THREADS, 0, (cudaStream_t)stream>>>(depth, valid, mm, stats, n);
     }
     return check_launch("depth_to_mm16");
 }
