@@ -69,6 +69,15 @@ typedef struct d360_group {
     const float *rel_t;         /* host (V,3) */
     const int32_t *offsets;     /* host (S,2) as (dx,dy) (E:60-65) */
     double trunc;               /* PatchSpec.cost_truncation */
+    const float *ref_ctx;       /* device, optional: reference patch context as one padded plane
+                                   (H + 2p, W + 2p, 4) f32 = (ray.x, ray.y, ray.z, luma) with
+                                   p = ref_ctx_pad wrapped columns / replicated rows (the sample
+                                   wrap / clamp rules of K:168-177 as data).  Written by
+                                   d360_build_ref_context.  With it (and p >= the patch reach) the
+                                   throughput eval / refine kernels stage a CTA's patch window in
+                                   shared memory with one TMA tile load (cp.async.bulk.tensor.2d)
+                                   instead of four scattered loads per window entry.  NULL: plain loads */
+    int32_t ref_ctx_pad;
 } d360_group;
 
 const char *d360_last_error(void);
@@ -123,6 +132,10 @@ int d360_run_patchmatch(const d360_group *g, float *depth, float *normal, float 
                         double depth_min,
                         double depth_max, uint8_t *valid_out, unsigned long long *n_evals,
                         void *stream);
+
+/* writes d360_group.ref_ctx from the (H,W,3) rays and the (H,W) reference luma */
+int d360_build_ref_context(const float *rays, const float *ref_gray, float *ctx, int height,
+                           int width, int pad, void *stream);
 
 /* replaces kernels.median_support_mask (K:613-647; caller E:634-648) */
 int d360_median_support_mask(const float *depth, const uint8_t *valid, int half,

@@ -37,6 +37,7 @@ class Group(C.Structure):
         ("nb64", c_void),
         ("rel_r", c_void), ("rel_t", c_void), ("offsets", c_void),
         ("trunc", C.c_double),
+        ("ref_ctx", c_void), ("ref_ctx_pad", C.c_int32),
     ]
 
 
@@ -51,6 +52,7 @@ _SIGNATURES = {
     "d360_refine_pass": (C.c_int, [C.POINTER(Group)] + [c_void] * 8 + [C.c_int, C.c_double, C.c_double, c_void]),
     "d360_run_patchmatch": (C.c_int, [C.POINTER(Group)] + [c_void] * 8 + [C.c_int, C.c_int, C.c_double,
                                                                          C.c_double, c_void, c_void, c_void]),
+    "d360_build_ref_context": (C.c_int, [c_void, c_void, c_void, C.c_int, C.c_int, C.c_int, c_void]),
     "d360_median_support_mask": (C.c_int, [c_void, c_void, C.c_int, C.c_double, c_void, C.c_int, C.c_int, c_void]),
     "d360_to_gray": (C.c_int, [c_void, C.c_int, c_void, C.c_int, C.c_int, c_void]),
     "d360_to_gray_padded": (C.c_int, [c_void, C.c_int, c_void, c_void, C.c_int, C.c_int, C.c_int, C.c_int, c_void]),

@@ -115,6 +115,17 @@ __global__ void k_random_init(float* depth, float* normal, float* cost, uint8_t*
     cost[i] = INFINITY;
 }
 
+// d360_group.ref_ctx: (ray, luma) per pixel with `pad` wrapped columns and replicated rows
+__global__ void k_build_ref_ctx(const float* __restrict__ rays, const float* __restrict__ gray, float4* __restrict__ ctx,
+                                int H, int W, int pad) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x, r = blockIdx.y;
+    const int PW = W + 2 * pad;
+    if (c >= PW) return;
+    const int x = pos_mod(c - pad, W), y = min(max(r - pad, 0), H - 1);
+    const size_t i = (size_t)y * W + x;
+    ctx[(size_t)r * PW + c] = make_float4(rays[3 * i], rays[3 * i + 1], rays[3 * i + 2], gray[i]);
+}
+
 __global__ void k_fill_u8(uint8_t* p, uint8_t v, size_t n) {
     size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
@@ -663,6 +674,21 @@ extern "C" int d360_median_support_mask(const float* depth, const uint8_t* valid
                                                                        height, width);
     }
     return check_launch("median_support_mask");
+}
+
+extern "C" int d360_build_ref_context(const float* rays, const float* ref_gray, float* ctx, int height, int width,
+                                      int pad, void* stream) {
+    if (pad < 0 || pad > 64 || height < 1 || width < 1) {
+        set_error("build_ref_context: bad size %dx%d pad %d", width, height, pad);
+        return 1;
+    }
+    dim3 grid((width + 2 * pad + 127) / 128, height + 2 * pad);
+    {
+        TraceScope ts_("build_ref_ctx", (cudaStream_t)stream);
+        k_build_ref_ctx<<<grid, 128, 0, (cudaStream_t)stream>>>(rays, ref_gray, reinterpret_cast<float4*>(ctx), height,
+                                                                width, pad);
+    }
+    return check_launch("build_ref_context");
 }
 
 extern "C" int d360_pole_mask(uint8_t* valid, double limit_deg, int height, int width, void* stream) {

@@ -108,6 +108,12 @@ int make_group_dev(const d360_group* g, GroupDev* out) {
     }
     d.nb_pad_x = g->nb_pad_x; d.nb_pad_y = g->nb_pad_y;
     d.nb64 = g->nb64;
+    d.ref_ctx = g->ref_ctx;
+    d.ref_ctx_pad = g->ref_ctx_pad;
+    if (d.ref_ctx != nullptr && (d.ref_ctx_pad < 0 || d.ref_ctx_pad > 64)) {
+        set_error("reference context pad %d outside [0, 64]", d.ref_ctx_pad);
+        return 1;
+    }
     int reach = 0;
     for (int k = 0; k < g->n_samples; ++k) {
         const int dx = g->offsets[2 * k], dy = g->offsets[2 * k + 1];

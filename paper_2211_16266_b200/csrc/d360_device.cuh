@@ -27,6 +27,8 @@ struct GroupDev {
     const float* ref_gray;
     const float* nb;
     const double* nb64;  // optional f64 copy of the padded neighbour planes (d360.h)
+    const float* ref_ctx;  // optional padded (ray, luma) plane of the reference (d360.h)
+    int ref_ctx_pad;
     float rel_r[D360_MAX_VIEWS][9];
     float rel_t[D360_MAX_VIEWS][3];
     signed char dx[D360_MAX_SAMPLES];

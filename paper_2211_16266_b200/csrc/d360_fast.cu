@@ -1,9 +1,46 @@
 // Host side shared by the throughput kernels (d360_fast_{eval,rb,refine}.cu): the FastGroup
 // parameter block.
+#include <string.h>
+
 #include "d360_fast.cuh"
 
 namespace d360 {
 namespace fast {
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        (void)cudaGetLastError();
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+void make_window_map(const GroupDev& gd, int reach, int tile_w, int tile_h, WindowMap* wm) {
+    wm->pad = -1;
+    memset(&wm->map, 0, sizeof(wm->map));
+    if (gd.ref_ctx == nullptr || gd.ref_ctx_pad < reach) return;
+    EncodeTiledFn enc = encode_tiled();
+    if (enc == nullptr) return;
+    const int p = gd.ref_ctx_pad;
+    const cuuint64_t dims[2] = {(cuuint64_t)4 * (gd.W + 2 * p), (cuuint64_t)(gd.H + 2 * p)};
+    const cuuint64_t strides[1] = {(cuuint64_t)4 * (gd.W + 2 * p) * sizeof(float)};
+    const cuuint32_t box[2] = {(cuuint32_t)(4 * (tile_w + 2 * reach)), (cuuint32_t)(tile_h + 2 * reach)};
+    const cuuint32_t estr[2] = {1, 1};
+    if (box[0] > 256 || box[1] > 256 || (reinterpret_cast<uintptr_t>(gd.ref_ctx) & 15) != 0) return;
+    const CUresult rc = enc(&wm->map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(gd.ref_ctx), dims, strides,
+                            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rc == CUDA_SUCCESS) wm->pad = p;
+}
 
 bool make_fast_group(const GroupDev& gd, FastGroup* out) {
     // regular grid?  S = ns^2, offsets (dx, dy) = stride * (i - half, j - half), dy outer (E:60-65)

@@ -22,6 +22,7 @@
 // instructions for the duplicated plane-depth chain and the per-lane view addressing, and the
 // smaller L1 next to 3 x 72 KB of shared memory: 20 % slower.  See DESIGN.md.)
 #pragma once
+#include <cuda.h>  // CUtensorMap (types only; the encoder is fetched through the runtime, no -lcuda)
 #include <math.h>
 
 #include "d360_device.cuh"
@@ -98,6 +99,8 @@ __host__ __device__ inline size_t tile_bytes(int tw, int th, int reach, bool com
     return ne * sizeof(float4) + ne * sizeof(double) * 3 * n_views;
 }
 
+__host__ __device__ inline size_t mbar_offset(size_t tile) { return (tile + 15) & ~(size_t)15; }
+
 template <class C>
 __device__ __forceinline__ Tile tile_setup(const FastGroup& g, unsigned char* smem, int x0, int y0, int th,
                                            bool compress, int keep) {
@@ -130,6 +133,73 @@ __device__ __forceinline__ Tile tile_setup(const FastGroup& g, unsigned char* sm
     t.ne = ne;
     t.sx = compress ? C::stride(g) / 2 : C::stride(g);
     t.sy = C::stride(g) * wwc;
+    return t;
+}
+
+// The same window staged by TMA (eval / refine, no colour compression): the reference's (ray, luma)
+// context lives in one padded float4 plane (d360_group.ref_ctx: wrapped columns, replicated rows,
+// so K:168-177's wrap / clamp is data), and the window of a CTA is exactly one box of it.  One
+// thread arms an mbarrier with the box's byte count and issues cp.async.bulk.tensor.2d; the TMA
+// unit writes the ww x hh float4 entries row-major to the start of shared memory, which is the
+// layout tile_setup produces, while the CTA's other warps are already through their index
+// arithmetic.  Then every thread derives R_v q of its entries from shared memory.
+struct WindowMap {
+    CUtensorMap map;  // 2-D f32 tensor (H + 2p rows, 4 (W + 2p) floats per row), box = (4 ww, hh)
+    int pad;          // p; < 0: no map, use tile_setup
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+template <class C>
+__device__ __forceinline__ Tile tile_setup_tma(const FastGroup& g, const WindowMap& wm, unsigned char* smem,
+                                               unsigned long long* mbar, int x0, int y0, int th) {
+    const int R = C::reach(g);
+    const int ww = TW + 2 * R, hh = th + 2 * R;
+    const int ne = ww * hh;
+    float4* qg = reinterpret_cast<float4*>(smem);
+    double* rq = reinterpret_cast<double*>(smem + (size_t)ne * sizeof(float4));
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)),
+                     "r"((unsigned)(ne * sizeof(float4)))
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                smem_u32(qg)),
+            "l"(reinterpret_cast<unsigned long long>(&wm.map)), "r"(4 * (x0 - R + wm.pad)), "r"(y0 - R + wm.pad),
+            "r"(smem_u32(mbar))
+            : "memory");
+    }
+    __syncthreads();  // the barrier is initialised for everyone
+    {
+        unsigned done = 0;
+        while (!done) {
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                : "=r"(done)
+                : "r"(smem_u32(mbar))
+                : "memory");
+        }
+    }
+    for (int e = threadIdx.x; e < ne; e += C::NT) {
+        const float4 q = qg[e];
+#pragma unroll
+        for (int v = 0; v < C::V; ++v) {
+            const float* r = g.rel_r[v];
+            rq[(v * 3 + 0) * ne + e] = (double)dot3_f32(r[0], r[1], r[2], q.x, q.y, q.z);
+            rq[(v * 3 + 1) * ne + e] = (double)dot3_f32(r[3], r[4], r[5], q.x, q.y, q.z);
+            rq[(v * 3 + 2) * ne + e] = (double)dot3_f32(r[6], r[7], r[8], q.x, q.y, q.z);
+        }
+    }
+    Tile t;
+    t.qg = qg;
+    t.rq = rq;
+    t.wwc = ww;
+    t.ne = ne;
+    t.sx = C::stride(g);
+    t.sy = C::stride(g) * ww;
     return t;
 }
 
@@ -468,6 +538,10 @@ __device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, i
 
 // host side, d360_fast.cu
 bool make_fast_group(const GroupDev& gd, FastGroup* out);
+// Tensor map of gd.ref_ctx with a (tile_w + 2 reach) x (tile_h + 2 reach) entry box; wm->pad = -1
+// when the group carries no context plane, its pad is smaller than the reach, or the driver has
+// no encoder (the kernels then fill the window with plain loads).
+void make_window_map(const GroupDev& gd, int reach, int tile_w, int tile_h, WindowMap* wm);
 
 template <typename K>
 static int prepare(K kernel, size_t smem) {

@@ -7,11 +7,14 @@ namespace fast {
 // A CTA covers TW x TH_FULL pixels, one thread per pixel.
 template <class C>
 __global__ void __launch_bounds__(C::NT, C::MINB)
-    k_eval(const __grid_constant__ FastGroup g, const float* __restrict__ depth, const float* __restrict__ normal,
-           float* __restrict__ cost_out) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    k_eval(const __grid_constant__ FastGroup g, const __grid_constant__ WindowMap wm, const float* __restrict__ depth,
+           const float* __restrict__ normal, float* __restrict__ cost_out) {
+    extern __shared__ __align__(128) unsigned char smem[];
     const int x0 = blockIdx.x * TW, y0 = blockIdx.y * C::TH_FULL;
-    const Tile t = tile_setup<C>(g, smem, x0, y0, C::TH_FULL, false, 0);
+    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(
+        smem + mbar_offset(tile_bytes(TW, C::TH_FULL, C::reach(g), false, C::V)));
+    const Tile t = wm.pad >= 0 ? tile_setup_tma<C>(g, wm, smem, mbar, x0, y0, C::TH_FULL)
+                               : tile_setup<C>(g, smem, x0, y0, C::TH_FULL, false, 0);
     __syncthreads();
     const int lx = threadIdx.x % TW, ly = threadIdx.x / TW;
     const int x = x0 + lx, y = y0 + ly;
@@ -34,13 +37,15 @@ int fast_eval(const GroupDev& gd, const float* depth, const float* normal, float
     FastGroup g;
     if (!make_fast_group(gd, &g)) return -1;
     D360_FAST_DISPATCH(gd.V, {
-        const size_t smem = tile_bytes(TW, C::TH_FULL, g.reach, false, gd.V);
+        const size_t smem = mbar_offset(tile_bytes(TW, C::TH_FULL, g.reach, false, gd.V)) + 16;
         if (smem > 200 * 1024) return -1;
         dim3 grid((gd.W + TW - 1) / TW, (gd.H + C::TH_FULL - 1) / C::TH_FULL);
+        WindowMap wm;
+        make_window_map(gd, g.reach, TW, C::TH_FULL, &wm);
         auto k = k_eval<C>;
         if (prepare(k, smem)) return 1;
         TraceScope ts_("eval_costs", s);
-        k<<<grid, C::NT, smem, s>>>(g, depth, normal, cost_out);
+        k<<<grid, C::NT, smem, s>>>(g, wm, depth, normal, cost_out);
     })
     return check_launch("eval_costs");
 }

@@ -11,16 +11,19 @@ __host__ __device__ inline size_t park_offset(size_t tile) { return (tile + 15) 
 
 template <class C>
 __global__ void __launch_bounds__(C::NT, C::MINB)
-    k_refine(const __grid_constant__ FastGroup g, const __grid_constant__ RefineTable tab, float* __restrict__ depth,
+    k_refine(const __grid_constant__ FastGroup g, const __grid_constant__ WindowMap wm,
+             const __grid_constant__ RefineTable tab, float* __restrict__ depth,
              float* __restrict__ normal, float* __restrict__ cost, unsigned char* __restrict__ flags,
              unsigned long long* n_evals) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];
     const int x0 = blockIdx.x * TW, y0 = blockIdx.y * C::TH_FULL;
-    const Tile t = tile_setup<C>(g, smem, x0, y0, C::TH_FULL, false, 0);
+    const size_t park_at = park_offset(tile_bytes(TW, C::TH_FULL, C::reach(g), false, C::V));
+    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(smem + park_at + 5 * sizeof(double) * C::NT);
+    const Tile t = wm.pad >= 0 ? tile_setup_tma<C>(g, wm, smem, mbar, x0, y0, C::TH_FULL)
+                               : tile_setup<C>(g, smem, x0, y0, C::TH_FULL, false, 0);
     // loop-carried hypothesis (d, n) and cost of each thread, parked here while a candidate is
     // evaluated: ten registers the evaluation's dependency chains can use instead
-    double* park = reinterpret_cast<double*>(smem + park_offset(tile_bytes(TW, C::TH_FULL, C::reach(g), false, C::V))) +
-                   threadIdx.x;
+    double* park = reinterpret_cast<double*>(smem + park_at) + threadIdx.x;
     __syncthreads();
     const int lx = threadIdx.x % TW, ly = threadIdx.x / TW;
     const int x = x0 + lx, y = y0 + ly;
@@ -109,13 +112,15 @@ int fast_refine(const GroupDev& gd, const RefineTable& tab, float* depth, float*
     FastGroup g;
     if (!make_fast_group(gd, &g)) return -1;
     D360_FAST_DISPATCH(gd.V, {
-        const size_t smem = park_offset(tile_bytes(TW, C::TH_FULL, g.reach, false, gd.V)) + 5 * sizeof(double) * C::NT;
+        const size_t smem = park_offset(tile_bytes(TW, C::TH_FULL, g.reach, false, gd.V)) + 5 * sizeof(double) * C::NT + 16;
         if (smem > 200 * 1024) return -1;
         dim3 grid((gd.W + TW - 1) / TW, (gd.H + C::TH_FULL - 1) / C::TH_FULL);
+        WindowMap wm;
+        make_window_map(gd, g.reach, TW, C::TH_FULL, &wm);
         auto k = k_refine<C>;
         if (prepare(k, smem)) return 1;
         TraceScope ts_("refine", s);
-        k<<<grid, C::NT, smem, s>>>(g, tab, depth, normal, cost, flags, n_evals);
+        k<<<grid, C::NT, smem, s>>>(g, wm, tab, depth, normal, cost, flags, n_evals);
     })
     return check_launch("refine_pass");
 }

@@ -222,6 +222,7 @@ class DeviceDepthPanorama:
 
 NB_PAD_X = 4  # wrapped columns each side of a neighbour plane (keeps rows 16-byte aligned)
 NB_PAD_Y = 1  # replicated rows above / below
+REF_CTX_PAD = 8  # wrapped columns / replicated rows of the reference context plane (>= any patch reach)
 
 
 def to_gray_device(image, device=None, out: torch.Tensor | None = None, pad=(0, 0),
@@ -334,6 +335,14 @@ class PreparedGroup:
                 for v, im in enumerate(imgs[1:]):
                     to_gray_device(im, self.device, out=self.nb_padded[v], pad=(NB_PAD_X, NB_PAD_Y),
                                    out64=self.nb64_padded[v])
+            # (ray, luma) of the reference as one padded float4 plane: the TMA source of the patch windows
+            self.ref_ctx = None
+            if self.precision == "mixed":
+                self.ref_ctx = torch.empty((h + 2 * REF_CTX_PAD, w + 2 * REF_CTX_PAD, 4), dtype=torch.float32,
+                                           device=self.device)
+                _lib.check(_lib.load().d360_build_ref_context(_ptr(self.cam_dev.rays32), _ptr(self.ref_gray),
+                                                              _ptr(self.ref_ctx), h, w, REF_CTX_PAD, _stream()),
+                           "build_ref_context")
         rel = [relative_transform(group.reference.pose, nb.pose) for nb in group.neighbors]
         self.rel_r = np.ascontiguousarray(np.stack([r for r, _ in rel]), dtype=np.float32)
         self.rel_t = np.ascontiguousarray(np.stack([t for _, t in rel]), dtype=np.float32)
@@ -342,7 +351,8 @@ class PreparedGroup:
             n_samples=len(self.offsets), top_k=self.top_k, precision=PRECISIONS[self.precision],
             rays=_ptr(self.cam_dev.rays32), ref_gray=_ptr(self.ref_gray), nb=_ptr(self.nb_padded), nb_pad_x=NB_PAD_X, nb_pad_y=NB_PAD_Y, nb64=_ptr(self.nb64_padded),
             rel_r=self.rel_r.ctypes.data, rel_t=self.rel_t.ctypes.data, offsets=self.offsets.ctypes.data,
-            trunc=float(spec.cost_truncation))
+            trunc=float(spec.cost_truncation),
+            ref_ctx=_ptr(self.ref_ctx) if self.ref_ctx is not None else 0, ref_ctx_pad=REF_CTX_PAD)
 
     @property
     def nb(self) -> torch.Tensor:

@@ -659,3 +659,32 @@ def test_metrics_match_reference(pkg):
                                                     np.ones((32, 64), bool)))
     assert [metrics.voxel_occupancy(z["points"], v) for v in (0.1, 0.5, 2.0)] == z["vox"].tolist()
     assert metrics.voxel_occupancy(np.zeros((0, 3))) == 0
+
+
+@pytest.mark.parametrize("name", ["hot_64x32_rot", "hot_256x128_c1"])
+def test_tma_window_staging_equals_plain_loads(pkg, name):
+    """eval / refine stage the patch window by one TMA tile load from the padded reference context
+    plane; dropping the plane from the group selects the plain-load path.  Same bits either way."""
+    p, engine, _, _ = pkg
+    z = load_golden(name)
+    group, spec, cam = make_group(p, z)
+    prep = engine.prepare_group(group, spec, precision="mixed")
+    assert prep.ref_ctx is not None and prep._struct.ref_ctx
+    init = engine.PlaneMap(cam, z["init_depth"], z["init_normal"], np.full(cam.shape, np.inf, np.float32),
+                           np.ones(cam.shape, bool), tuple(z["depth_range"]))
+    out = []
+    for use_tma in (True, False):
+        if not use_tma:
+            prep._struct.ref_ctx = 0
+        pm = engine.DevicePlaneMap.from_host(init)
+        engine.run_patchmatch_device(prep, pm, 2, int(z["seed"]))
+        out.append((pm.depth.cpu().numpy(), pm.normal.cpu().numpy(), pm.cost.cpu().numpy()))
+    for a, b in zip(*out):
+        assert np.array_equal(a, b)
+    # the plane itself: wrapped columns, replicated rows
+    ctx = prep.ref_ctx.cpu().numpy()
+    pad = engine.REF_CTX_PAD
+    h, w = cam.shape
+    ys = np.clip(np.arange(-pad, h + pad), 0, h - 1)
+    xs = np.arange(-pad, w + pad) % w
+    assert np.array_equal(ctx[..., :3], z["rays"][ys][:, xs]) and np.array_equal(ctx[..., 3], z["ref_gray"][ys][:, xs])
