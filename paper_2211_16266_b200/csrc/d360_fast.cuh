@@ -312,7 +312,8 @@ __device__ __forceinline__ void project_uv(const FastGroup& g, const double (&tx
 // are issued; all offsets are 32-bit element indices from one base.
 template <int VT>
 __device__ __forceinline__ void gather_bilinear(const FastGroup& g, const double2* __restrict__ nb,
-                                                const float (&pu)[VT], const float (&pv)[VT], double (&val)[VT]) {
+                                                unsigned plane_stride, const float (&pu)[VT], const float (&pv)[VT],
+                                                double (&val)[VT]) {
     const float MAGIC = 12582912.0f;  // 1.5 * 2^23: (x + MAGIC) rounded towards -inf is floor(x) + MAGIC
     float fl_u[VT], fl_v[VT];
 #pragma unroll
@@ -326,7 +327,7 @@ __device__ __forceinline__ void gather_bilinear(const FastGroup& g, const double
     double2 r0[VT], r1[VT];  // { value, value(x+1) - value }
 #pragma unroll
     D360_FORV {
-        const double2* __restrict__ row0 = nb + (size_t)v * g.plane32;  // uniform per view
+        const double2* __restrict__ row0 = nb + (size_t)v * plane_stride;  // uniform per view
         const double2* __restrict__ row1 = row0 + g.pitch;
         r0[v] = __ldg(row0 + idx[v]);
         r1[v] = __ldg(row1 + idx[v]);
@@ -421,7 +422,7 @@ __device__ __forceinline__ void accumulate_views(const FastGroup& g, const Tile&
                     tz[v] = fma(lam, rqe[(v * 3 + 2) * t.ne], g.rel_t[V0 + v][2]);
                 }
                 project_uv<VC>(g, tx, ty, tz, pu, pv);
-                gather_bilinear<VC>(g, nb, pu, pv, val);
+                gather_bilinear<VC>(g, nb, g.plane32, pu, pv, val);
 #pragma unroll
                 for (int v = 0; v < VC; ++v) {
                     s0[v] += val[v];
@@ -439,7 +440,7 @@ __device__ __forceinline__ void accumulate_views(const FastGroup& g, const Tile&
                     tz[v] = fma(lam, rqe[((VC + v) * 3 + 2) * t.ne], g.rel_t[V0 + VC + v][2]);
                 }
                 project_uv<VR>(g, tx, ty, tz, pu, pv);
-                gather_bilinear<VR>(g, nb + (size_t)VC * g.plane32, pu, pv, val);
+                gather_bilinear<VR>(g, nb + (size_t)VC * g.plane32, g.plane32, pu, pv, val);
 #pragma unroll
                 for (int v = 0; v < VR; ++v) {
                     s0[VC + v] += val[v];
@@ -451,6 +452,74 @@ __device__ __forceinline__ void accumulate_views(const FastGroup& g, const Tile&
         e = e_next;
         lam = lam_next;
         rv = rv_next;
+    }
+}
+
+// The same sums for ONE view (the second pass of an early-out evaluation, see cand_cost), two
+// samples per trip: with a single view there is only one projection chain per sample, so two
+// consecutive samples are staged side by side to give the warp two chains in flight.  The sums
+// take the samples in the same order as accumulate_views.
+template <class C, typename HT, int V0>
+__device__ __forceinline__ void accumulate_one_view(const FastGroup& g, const Tile& t, int ce, double num, HT nx, HT ny,
+                                                    HT nz, double& s0, double& ss0, double& rs0) {
+    s0 = ss0 = rs0 = 0.0;
+    const double2* __restrict__ nb = reinterpret_cast<const double2*>(g.nb64) + (size_t)V0 * g.plane32;
+    auto plane_depth = [&](int es, double& lam, double& rv) {
+        const float4 q = t.qg[es];
+        double dn;
+        if constexpr (sizeof(HT) == 4) {
+            dn = (double)fminf(dot3_f32(nx, ny, nz, q.x, q.y, q.z), g.den_lim);
+        } else {
+            const double den = fma(nz, (double)q.z, fma(ny, (double)q.y, nx * (double)q.x));
+            dn = den > g.neg_par_eps ? g.neg_par_eps : den;
+        }
+        lam = num * rcp3(dn);
+        rv = (double)q.w;
+    };
+    const int ns = C::ns(g);
+    const int half = (ns - 1) / 2;
+    const int n_samples = ns * ns;
+    const int row_wrap = t.sy - ns * t.sx;
+    const double* rq0 = t.rq + V0 * 3 * t.ne;
+    int e = ce - half * (t.sx + t.sy), col = 0;
+    auto next_entry = [&](int cur) {
+        int nxt = cur + t.sx;
+        if (++col == ns) { col = 0; nxt += row_wrap; }
+        return nxt;
+    };
+    int k = 0;
+#pragma unroll 1
+    for (; k + 1 < n_samples; k += 2) {
+        const int ea = e, eb = next_entry(ea);
+        e = next_entry(eb);
+        double lam[2], rv[2], tx[2], ty[2], tz[2], val[2];
+        float pu[2], pv[2];
+        plane_depth(ea, lam[0], rv[0]);
+        plane_depth(eb, lam[1], rv[1]);
+        tx[0] = fma(lam[0], rq0[0 * t.ne + ea], g.rel_t[V0][0]); tx[1] = fma(lam[1], rq0[0 * t.ne + eb], g.rel_t[V0][0]);
+        ty[0] = fma(lam[0], rq0[1 * t.ne + ea], g.rel_t[V0][1]); ty[1] = fma(lam[1], rq0[1 * t.ne + eb], g.rel_t[V0][1]);
+        tz[0] = fma(lam[0], rq0[2 * t.ne + ea], g.rel_t[V0][2]); tz[1] = fma(lam[1], rq0[2 * t.ne + eb], g.rel_t[V0][2]);
+        project_uv<2>(g, tx, ty, tz, pu, pv);
+        gather_bilinear<2>(g, nb, 0u, pu, pv, val);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            s0 += val[j];
+            ss0 = fma(val[j], val[j], ss0);
+            rs0 = fma(rv[j], val[j], rs0);
+        }
+    }
+    if (k < n_samples) {
+        double lam, rv, tx[1], ty[1], tz[1], val[1];
+        float pu[1], pv[1];
+        plane_depth(e, lam, rv);
+        tx[0] = fma(lam, rq0[0 * t.ne + e], g.rel_t[V0][0]);
+        ty[0] = fma(lam, rq0[1 * t.ne + e], g.rel_t[V0][1]);
+        tz[0] = fma(lam, rq0[2 * t.ne + e], g.rel_t[V0][2]);
+        project_uv<1>(g, tx, ty, tz, pu, pv);
+        gather_bilinear<1>(g, nb, 0u, pu, pv, val);
+        s0 += val[0];
+        ss0 = fma(val[0], val[0], ss0);
+        rs0 = fma(rv, val[0], rs0);
     }
 }
 
@@ -521,9 +590,9 @@ __device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, i
             }
         }
         {
-            double s0[1], ss0[1], rs0[1];
-            accumulate_views<C, HT, VA, 1>(g, t, ce, num, nx, ny, nz, bad, s0, ss0, rs0);
-            cv[VA] = view_cost(g, s0[0], ss0[0], rs0[0], mr, sr);
+            double s0, ss0, rs0;
+            accumulate_one_view<C, HT, VA>(g, t, ce, num, nx, ny, nz, s0, ss0, rs0);
+            cv[VA] = view_cost(g, s0, ss0, rs0, mr, sr);
         }
     } else {
         double s0[VT], ss0[VT], rs0[VT];
