@@ -310,7 +310,7 @@ __device__ __forceinline__ void project_uv(const FastGroup& g, const double (&tx
 // cost of low-texture patches, measured).  floor by the 1.5 * 2^23 magic add; the element index
 // is formed in f32 (exact below 2^23) and read out of the mantissa, so no F2I / I2F conversions
 // are issued; all offsets are 32-bit element indices from one base.
-template <int VT>
+template <int VT, int PERIOD = VT>
 __device__ __forceinline__ void gather_bilinear(const FastGroup& g, const double2* __restrict__ nb,
                                                 unsigned plane_stride, const float (&pu)[VT], const float (&pv)[VT],
                                                 double (&val)[VT]) {
@@ -327,7 +327,7 @@ __device__ __forceinline__ void gather_bilinear(const FastGroup& g, const double
     double2 r0[VT], r1[VT];  // { value, value(x+1) - value }
 #pragma unroll
     D360_FORV {
-        const double2* __restrict__ row0 = nb + (size_t)v * plane_stride;  // uniform per view
+        const double2* __restrict__ row0 = nb + (size_t)(v % PERIOD) * plane_stride;  // uniform per view
         const double2* __restrict__ row1 = row0 + g.pitch;
         r0[v] = __ldg(row0 + idx[v]);
         r1[v] = __ldg(row1 + idx[v]);
@@ -455,23 +455,29 @@ __device__ __forceinline__ void accumulate_views(const FastGroup& g, const Tile&
     }
 }
 
-// The same sums for ONE view (the second pass of an early-out evaluation, see cand_cost), two
-// samples per trip: with a single view there is only one projection chain per sample, so two
-// consecutive samples are staged side by side to give the warp two chains in flight.  The sums
-// take the samples in the same order as accumulate_views.
-template <class C, typename HT, int V0>
-__device__ __forceinline__ void accumulate_one_view(const FastGroup& g, const Tile& t, int ce, double num, HT nx, HT ny,
-                                                    HT nz, double& s0, double& ss0, double& rs0) {
-    s0 = ss0 = rs0 = 0.0;
+// The same sums for NV <= 2 views, two samples per trip: with one or two views there are only
+// one or two projection chains per sample, so two consecutive samples are staged side by side
+// to give the warp 2 NV chains in flight.  The sums take the samples in the same order as
+// accumulate_views, so the results are identical.
+template <class C, typename HT, int V0, int NV>
+__device__ __forceinline__ void accumulate_views_2s(const FastGroup& g, const Tile& t, int ce, double num, HT nx, HT ny,
+                                                    HT nz, bool& bad, double (&s0)[NV], double (&ss0)[NV],
+                                                    double (&rs0)[NV]) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) s0[v] = ss0[v] = rs0[v] = 0.0;
     const double2* __restrict__ nb = reinterpret_cast<const double2*>(g.nb64) + (size_t)V0 * g.plane32;
     auto plane_depth = [&](int es, double& lam, double& rv) {
         const float4 q = t.qg[es];
         double dn;
         if constexpr (sizeof(HT) == 4) {
-            dn = (double)fminf(dot3_f32(nx, ny, nz, q.x, q.y, q.z), g.den_lim);
+            const float den = dot3_f32(nx, ny, nz, q.x, q.y, q.z);
+            bad = bad || (den > g.den_lim);
+            dn = (double)fminf(den, g.den_lim);
         } else {
             const double den = fma(nz, (double)q.z, fma(ny, (double)q.y, nx * (double)q.x));
-            dn = den > g.neg_par_eps ? g.neg_par_eps : den;
+            const bool par = den > g.neg_par_eps;
+            bad = bad || par;
+            dn = par ? g.neg_par_eps : den;
         }
         lam = num * rcp3(dn);
         rv = (double)q.w;
@@ -490,36 +496,53 @@ __device__ __forceinline__ void accumulate_one_view(const FastGroup& g, const Ti
     int k = 0;
 #pragma unroll 1
     for (; k + 1 < n_samples; k += 2) {
-        const int ea = e, eb = next_entry(ea);
-        e = next_entry(eb);
-        double lam[2], rv[2], tx[2], ty[2], tz[2], val[2];
-        float pu[2], pv[2];
-        plane_depth(ea, lam[0], rv[0]);
-        plane_depth(eb, lam[1], rv[1]);
-        tx[0] = fma(lam[0], rq0[0 * t.ne + ea], g.rel_t[V0][0]); tx[1] = fma(lam[1], rq0[0 * t.ne + eb], g.rel_t[V0][0]);
-        ty[0] = fma(lam[0], rq0[1 * t.ne + ea], g.rel_t[V0][1]); ty[1] = fma(lam[1], rq0[1 * t.ne + eb], g.rel_t[V0][1]);
-        tz[0] = fma(lam[0], rq0[2 * t.ne + ea], g.rel_t[V0][2]); tz[1] = fma(lam[1], rq0[2 * t.ne + eb], g.rel_t[V0][2]);
-        project_uv<2>(g, tx, ty, tz, pu, pv);
-        gather_bilinear<2>(g, nb, 0u, pu, pv, val);
+        int es[2];
+        es[0] = e;
+        es[1] = next_entry(es[0]);
+        e = next_entry(es[1]);
+        double lam[2], rv[2], tx[2 * NV], ty[2 * NV], tz[2 * NV], val[2 * NV];
+        float pu[2 * NV], pv[2 * NV];
+        plane_depth(es[0], lam[0], rv[0]);
+        plane_depth(es[1], lam[1], rv[1]);
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-            s0 += val[j];
-            ss0 = fma(val[j], val[j], ss0);
-            rs0 = fma(rv[j], val[j], rs0);
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                tx[j * NV + v] = fma(lam[j], rq0[(v * 3 + 0) * t.ne + es[j]], g.rel_t[V0 + v][0]);
+                ty[j * NV + v] = fma(lam[j], rq0[(v * 3 + 1) * t.ne + es[j]], g.rel_t[V0 + v][1]);
+                tz[j * NV + v] = fma(lam[j], rq0[(v * 3 + 2) * t.ne + es[j]], g.rel_t[V0 + v][2]);
+            }
+        }
+        project_uv<2 * NV>(g, tx, ty, tz, pu, pv);
+        gather_bilinear<2 * NV, NV>(g, nb, g.plane32, pu, pv, val);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                s0[v] += val[j * NV + v];
+                ss0[v] = fma(val[j * NV + v], val[j * NV + v], ss0[v]);
+                rs0[v] = fma(rv[j], val[j * NV + v], rs0[v]);
+            }
         }
     }
     if (k < n_samples) {
-        double lam, rv, tx[1], ty[1], tz[1], val[1];
-        float pu[1], pv[1];
+        double lam, rv, tx[NV], ty[NV], tz[NV], val[NV];
+        float pu[NV], pv[NV];
         plane_depth(e, lam, rv);
-        tx[0] = fma(lam, rq0[0 * t.ne + e], g.rel_t[V0][0]);
-        ty[0] = fma(lam, rq0[1 * t.ne + e], g.rel_t[V0][1]);
-        tz[0] = fma(lam, rq0[2 * t.ne + e], g.rel_t[V0][2]);
-        project_uv<1>(g, tx, ty, tz, pu, pv);
-        gather_bilinear<1>(g, nb, 0u, pu, pv, val);
-        s0 += val[0];
-        ss0 = fma(val[0], val[0], ss0);
-        rs0 = fma(rv, val[0], rs0);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            tx[v] = fma(lam, rq0[(v * 3 + 0) * t.ne + e], g.rel_t[V0 + v][0]);
+            ty[v] = fma(lam, rq0[(v * 3 + 1) * t.ne + e], g.rel_t[V0 + v][1]);
+            tz[v] = fma(lam, rq0[(v * 3 + 2) * t.ne + e], g.rel_t[V0 + v][2]);
+        }
+        project_uv<NV>(g, tx, ty, tz, pu, pv);
+        gather_bilinear<NV>(g, nb, g.plane32, pu, pv, val);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            s0[v] += val[v];
+            ss0[v] = fma(val[v], val[v], ss0[v]);
+            rs0[v] = fma(rv, val[v], rs0[v]);
+        }
     }
 }
 
@@ -590,16 +613,19 @@ __device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, i
             }
         }
         {
-            double s0, ss0, rs0;
-            accumulate_one_view<C, HT, VA>(g, t, ce, num, nx, ny, nz, s0, ss0, rs0);
-            cv[VA] = view_cost(g, s0, ss0, rs0, mr, sr);
+            double s0[1], ss0[1], rs0[1];
+            bool bad_again = false;  // same samples as the first pass: nothing new
+            accumulate_views_2s<C, HT, VA, 1>(g, t, ce, num, nx, ny, nz, bad_again, s0, ss0, rs0);
+            cv[VA] = view_cost(g, s0[0], ss0[0], rs0[0], mr, sr);
         }
     } else {
-        double s0[VT], ss0[VT], rs0[VT];
-        accumulate_views<C, HT, 0, VT>(g, t, ce, num, nx, ny, nz, bad, s0, ss0, rs0);
-        if (bad) return trunc;
+        {
+            double s0[VT], ss0[VT], rs0[VT];
+            accumulate_views<C, HT, 0, VT>(g, t, ce, num, nx, ny, nz, bad, s0, ss0, rs0);
+            if (bad) return trunc;
 #pragma unroll
-        for (int v = 0; v < VT; ++v) cv[v] = view_cost(g, s0[v], ss0[v], rs0[v], mr, sr);
+            for (int v = 0; v < VT; ++v) cv[v] = view_cost(g, s0[v], ss0[v], rs0[v], mr, sr);
+        }
     }
     const double total = aggregate<VT>(cv, g.top_k);
     return total == total ? total : trunc;  // NaN only from the unguarded polar singularities
