@@ -688,3 +688,51 @@ def test_tma_window_staging_equals_plain_loads(pkg, name):
     ys = np.clip(np.arange(-pad, h + pad), 0, h - 1)
     xs = np.arange(-pad, w + pad) % w
     assert np.array_equal(ctx[..., :3], z["rays"][ys][:, xs]) and np.array_equal(ctx[..., 3], z["ref_gray"][ys][:, xs])
+
+
+def test_c4_size_fast_vs_literal_and_fusion(pkg):
+    """BASELINE config C4 size (3840x1920, 6 neighbour views, 11x11 window at stride 2, fusion):
+    the throughput kernels against the literal-policy kernels on the same hypotheses (the padded
+    plane is 7.4 M texels, close to the 2^23 limit of the f32 tap index), then fusion properties."""
+    p, engine, pipeline, synth = pkg
+    cam = p.EquirectCamera(3840, 1920)
+    scene = synth.default_scene("corridor")
+    group, gt = synth.make_group(scene, cam, n_views=6)
+    spec, dr = engine.PatchSpec(), (0.5, 16.0)
+    fast = engine.prepare_group(group, spec, precision="mixed")
+    pm = engine.DevicePlaneMap.empty(cam, dr)
+    engine.random_init_device(pm, dr, 5, "philox")
+    # near-ground-truth hypotheses on half of the rows: low costs are where a one-ulp (u, v) error shows
+    gt_t = torch.from_numpy(gt).cuda()
+    rays = fast.cam_dev.rays32
+    pm.depth[::2] = gt_t[::2] * 1.003
+    engine.evaluate_costs_device(fast, pm)
+    c_fast = pm.cost.clone()
+    lit = engine.prepare_group(group, spec, precision="exact")
+    engine.evaluate_costs_device(lit, pm)
+    c_lit = pm.cost
+    ok = (c_fast.double() - c_lit.double()).abs() <= 1e-4 * c_lit.double() + 1e-7
+    assert ok.all(), (int((~ok).sum()), float((c_fast - c_lit).abs().max()))
+    assert (c_lit < 1.2).float().mean() > 0.3 and float(c_lit[::2].median()) < float(c_lit[1::2].median())
+    del lit
+    # one full iteration runs and never raises a cost
+    pm2, pano = engine.run_patchmatch_device(fast, pm, 1, 5, check_valid=False)
+    assert (pm2.cost <= c_lit).all()
+    # fusion at this size: a frame fused against an identical newer frame is erased completely,
+    # against a far-away one it survives, and the surviving points back-project onto the depth map
+    valid = torch.ones(cam.shape, dtype=torch.uint8, device="cuda")
+    img = torch.from_numpy(group.reference.image).cuda()
+    pose0 = group.reference.pose
+    fb = pipeline.FusionBuffer(cam, pipeline.FusionConfig(buffer=2))
+    a = pipeline.DeviceDepthResult(0, engine.DeviceDepthPanorama(cam, gt_t, valid), pose0, img)
+    assert fb.push_device(a) is None
+    out = fb.push_device(pipeline.DeviceDepthResult(1, engine.DeviceDepthPanorama(cam, gt_t, valid), pose0, img))
+    assert out is not None and len(out) == 0
+    far = p.RigidPose(np.eye(3), pose0.translation + np.array([0.0, 0.0, 6.0]))
+    none_valid = torch.zeros(cam.shape, dtype=torch.uint8, device="cuda")
+    out = fb.push_device(pipeline.DeviceDepthResult(2, engine.DeviceDepthPanorama(cam, gt_t, none_valid), far, img))
+    assert len(out) == cam.width * cam.height  # nothing to be a duplicate of
+    pts = out.points[:: 9973].cpu().numpy()
+    u, v, r = pipeline.project_points(cam, pose0, pts)
+    px, py = np.rint(u).astype(int) % cam.width, np.clip(np.rint(v).astype(int), 0, cam.height - 1)
+    assert np.abs(r - gt[py, px]).max() < 1e-5

@@ -140,3 +140,39 @@ def test_two_shards_reproduce_single_stream():
     ref_batches += fb.flush_device()
     ref = gather_cloud(ref_batches)
     assert np.array_equal(one.points, ref.points) and np.array_equal(one.source_ids, ref.source_ids)
+
+
+@pytest.mark.gpu
+def test_c5_sequence_sharding_full_size():
+    """BASELINE config C5: 64 keyframes at 1920x960 with 4 neighbour views, sharded 1 / 8 ways
+    (the 8 shards run one after the other on the one GPU): the gathered cloud is the
+    single-stream cloud bit for bit, oldest keyframe first."""
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2211_16266_b200 as p
+    from paper_2211_16266_b200 import engine, pipeline, synth
+    from paper_2211_16266_b200.sequence import densify_shard, gather_cloud, plan_shards
+
+    cam = p.EquirectCamera(1920, 960)
+    scene = synth.default_scene("corridor")
+    kfs = []
+    for k in range(64):
+        pose = p.RigidPose(np.eye(3), np.array([0.2, -0.1, -4.7 + 0.15 * k]))
+        img, _ = synth.render_scene(scene, cam, pose)
+        kfs.append(p.Keyframe(id=k, image=img, pose=pose))
+    groups = [p.StereoGroup(reference=kfs[i], neighbors=(kfs[i - 1], kfs[i + 1], kfs[i - 2], kfs[i + 2]), camera=cam)
+              for i in range(2, 62)]
+    ccfg, fcfg = pipeline.ConsistencyConfig(), pipeline.FusionConfig()
+
+    def run(world):
+        clouds = []
+        for plan in plan_shards(len(groups), world):
+            stage = pipeline.DepthStage(cam, engine.PatchSpec(), (0.5, 16.0), 1, 0, warp=False, init_rng="philox")
+            clouds.append(gather_cloud(densify_shard(groups, plan, stage, ccfg, fcfg)))
+        return pipeline.FusedCloud.concat(clouds)
+
+    one, eight = run(1), run(8)
+    assert len(one) > 100000
+    assert np.array_equal(one.points, eight.points) and np.array_equal(one.colors, eight.colors)
+    assert np.array_equal(one.source_ids, eight.source_ids)
+    assert np.all(np.diff(one.source_ids) >= 0)
