@@ -245,9 +245,59 @@ def io_metrics_case():
     print("io/metrics ok", len(ply), len(png), comp["per_keyframe"], acc, vox)
 
 
+def offline_case():
+    """run_offline on the 20-keyframe 64x32 room of the reference's own pipeline test
+    (tests/test_pipeline.py:279-296): inputs, every view-filter decision, report, filtered maps."""
+    import tempfile
+
+    from densify360.config import load_config
+    from densify360.dataset import load_dataset
+    from densify360.pipeline import run_offline
+    from densify360.synth import make_dataset
+    from densify360.viewfilter import view_filter_accept
+
+    with tempfile.TemporaryDirectory() as d:
+        make_dataset(default_scene("box"), keyframes=20, sparse_density=150, out_dir=d, camera=EquirectCamera(64, 32),
+                     seed=5)
+        ds = load_dataset(d)
+        cfg = load_config(overrides={"patchmatch.iterations": 4, "patchmatch.depth_max": 8.0,
+                                     "consistency.rel_depth_tol": 0.05, "processing.threaded": False})
+        kfs = list(ds.keyframes())
+        # a second landmark layout that makes the view filter reject: drop most shared landmarks of some frames
+        res = run_offline(ds, cfg)
+        latest, decisions = None, []
+        for kf in kfs:
+            if latest is None:
+                decisions.append((1, 1.0, 0))
+                latest = kf
+                continue
+            dec = view_filter_accept(kf, latest, cfg.viewfilter)
+            decisions.append((int(dec.accepted), dec.fraction, dec.common_points))
+            if dec.accepted:
+                latest = kf
+    rep = res.report
+    ids = sorted(res.depths)
+    np.savez_compressed(
+        OUT / "offline_64x32.npz", images=np.stack([k.image for k in kfs]),
+        rotations=np.stack([k.pose.rotation for k in kfs]), translations=np.stack([k.pose.translation for k in kfs]),
+        sparse=np.stack([k.sparse_points for k in kfs]), decisions=np.array(decisions),
+        vf=np.array([cfg.viewfilter.theta_min, cfg.viewfilter.theta_max, cfg.viewfilter.accept_fraction]),
+        keyframes_total=rep["keyframes_total"], keyframes_accepted=rep["keyframes_accepted"],
+        depth_jobs=rep["depth_jobs"], fused_points=rep["fused_points"],
+        comp_series=np.array(rep["completeness"]["per_keyframe"]), comp_mean=rep["completeness"]["mean"],
+        depth_ids=np.array(ids), depths=np.stack([res.depths[i].pano.depth for i in ids]),
+        valids=np.stack([res.depths[i].pano.valid for i in ids]), cloud_ids=res.cloud.source_ids,
+        report_keys=np.array(sorted(rep)))
+    print("offline ok", rep["keyframes_total"], rep["keyframes_accepted"], rep["depth_jobs"], rep["fused_points"],
+          rep["completeness"]["mean"], ids, decisions[:4])
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["io"]:
         io_metrics_case()
+        sys.exit(0)
+    if sys.argv[1:] == ["offline"]:
+        offline_case()
         sys.exit(0)
     ident = lambda z: RigidPose(rotation=np.eye(3), translation=np.array([0.0, 0.0, z]))
     hot_path_case("hot_64x32_ident", 64, 3, [ident(-0.15), ident(0.0), ident(0.15)], PatchSpec(), 7, True)
@@ -259,3 +309,4 @@ if __name__ == "__main__":
     stage_case()
     misc_case()
     io_metrics_case()
+    offline_case()

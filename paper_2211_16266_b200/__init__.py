@@ -32,6 +32,10 @@ _PIPELINE_NAMES = {
 }
 
 
+_OFFLINE_NAMES = {"ViewFilterConfig", "ViewFilterDecision", "view_filter_accept", "KeyframeBuffer", "PipelineResult",
+                  "run_offline"}
+
+
 def __getattr__(name):
     # engine / pipeline import torch; keep `import paper_2211_16266_b200` light.
     if name in _ENGINE_NAMES:
@@ -42,4 +46,8 @@ def __getattr__(name):
         from . import pipeline
 
         return getattr(pipeline, name)
+    if name in _OFFLINE_NAMES:
+        from . import offline
+
+        return getattr(offline, name)
     raise AttributeError(f"module {__name__!r} has no attribute {name!r}")

@@ -371,6 +371,8 @@ class StreamingDensifier:
         self._window: deque = deque()                        # DeviceDepthResult
         self._fusion = FusionBuffer(camera, fusion, self.device) if fusion is not None else None
         self._last_id = None
+        self.jobs = 0       # depth jobs run so far
+        self._images = {}   # host image of every reference whose output is still pending
 
     def push(self, keyframe: Keyframe) -> list:
         """Feed the next keyframe (ids strictly increasing); returns the outputs that
@@ -391,6 +393,8 @@ class StreamingDensifier:
         prep = PreparedGroup(group, self.stage.spec, top_k=self.stage.top_k, precision=self.stage.precision,
                              device=self.device, device_keyframes=[self._frames[i][1] for i in picks])
         self._window.append(self.stage.process_device(prep))
+        self.jobs += 1
+        self._images[group.reference.id] = group.reference.image
         if len(self._window) < self.consistency.window:
             return []
         frames = list(self._window)
@@ -404,6 +408,12 @@ class StreamingDensifier:
             batch = self._fusion.push_device(DeviceDepthResult(target.id, pano, target.pose, target.image))
             out.cloud = None if batch is None else batch.to_host()
         return [out]
+
+    def image_of(self, keyframe_id: int):
+        """Host image of a reference keyframe whose StreamOutput was just returned (handed over once)."""
+        for old in [k for k in self._images if k < keyframe_id]:
+            del self._images[old]  # frames the consistency window left behind without an output
+        return self._images.pop(keyframe_id)
 
     def finish(self) -> list:
         """Flush the fusion FIFO; frames still inside the consistency window are
