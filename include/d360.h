@@ -74,7 +74,7 @@ typedef struct d360_group {
                                    p = ref_ctx_pad wrapped columns / replicated rows (the sample
                                    wrap / clamp rules of K:168-177 as data).  Written by
                                    d360_build_ref_context.  With it (and p >= the patch reach) the
-                                   throughput eval / refine kernels stage a CTA's patch window in
+                                   throughput kernels stage a CTA's patch window in
                                    shared memory with one TMA tile load (cp.async.bulk.tensor.2d)
                                    instead of four scattered loads per window entry.  NULL: plain loads */
     int32_t ref_ctx_pad;

@@ -40,25 +40,94 @@ struct RbQueue {
     unsigned short items[NT * 8]; // p * 8 + j
     int warp_totals[NT / 32];
     int total, next;
+    unsigned long long mbar;      // TMA completion barrier of the window load
 };
 
-__host__ __device__ inline size_t rb_queue_offset(size_t tile) { return (tile + 15) & ~(size_t)15; }
+// 128-byte aligned: the cost array doubles as the TMA landing area of the uncompressed window
+__host__ __device__ inline size_t rb_queue_offset(size_t tile) { return (tile + 127) & ~(size_t)127; }
+
+// Colour-compressed window from one TMA box: the full (TW + 2R) x (TH_RB + 2R) float4 window lands
+// in `stage` (the queue's cost array, not needed before phase 2), then every thread copies the
+// entries of the pass's colour to their compressed slots and derives R_v q for them.
+template <class C>
+__device__ __forceinline__ Tile tile_setup_tma_compressed(const FastGroup& g, const WindowMap& wm, unsigned char* smem,
+                                                          float4* stage, unsigned long long* mbar, int x0, int y0,
+                                                          int keep) {
+    const int R = C::reach(g);
+    const int ww = TW + 2 * R, hh = C::TH_RB + 2 * R;
+    const int wwc = ww / 2;
+    const int ne = wwc * hh;
+    float4* qg = reinterpret_cast<float4*>(smem);
+    double* rq = reinterpret_cast<double*>(smem + (size_t)ne * sizeof(float4));
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)),
+                     "r"((unsigned)(ww * hh * sizeof(float4)))
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                smem_u32(stage)),
+            "l"(reinterpret_cast<unsigned long long>(&wm.map)), "r"(4 * (x0 - R + wm.pad)), "r"(y0 - R + wm.pad),
+            "r"(smem_u32(mbar))
+            : "memory");
+    }
+    __syncthreads();
+    {
+        unsigned done = 0;
+        while (!done) {
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                : "=r"(done)
+                : "r"(smem_u32(mbar))
+                : "memory");
+        }
+    }
+    for (int e = threadIdx.x; e < ne; e += C::NT) {
+        const int j = e / wwc, ic = e - j * wwc;
+        const int i = 2 * ic + ((keep + j) & 1);
+        const float4 q = stage[j * ww + i];
+        qg[e] = q;
+#pragma unroll
+        for (int v = 0; v < C::V; ++v) {
+            const float* r = g.rel_r[v];
+            rq[(v * 3 + 0) * ne + e] = (double)dot3_f32(r[0], r[1], r[2], q.x, q.y, q.z);
+            rq[(v * 3 + 1) * ne + e] = (double)dot3_f32(r[3], r[4], r[5], q.x, q.y, q.z);
+            rq[(v * 3 + 2) * ne + e] = (double)dot3_f32(r[6], r[7], r[8], q.x, q.y, q.z);
+        }
+    }
+    Tile t;
+    t.qg = qg;
+    t.rq = rq;
+    t.wwc = wwc;
+    t.ne = ne;
+    t.sx = C::stride(g) / 2;
+    t.sy = C::stride(g) * wwc;
+    return t;
+}
 
 template <class C>
 __global__ void __launch_bounds__(C::NT, C::MINB)
-    k_red_black(const __grid_constant__ FastGroup g, int parity, const float* __restrict__ depth_in,
+    k_red_black(const __grid_constant__ FastGroup g, const __grid_constant__ WindowMap wm, int parity,
+                const float* __restrict__ depth_in,
                 const float* __restrict__ normal_in, const float* __restrict__ cost_in, float* __restrict__ depth_out,
                 float* __restrict__ normal_out, float* __restrict__ cost_out,
                 const unsigned char* __restrict__ flags_in, unsigned char* __restrict__ flags_out,
                 unsigned long long* n_evals) {
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];
     constexpr int NT = C::NT;
     const int x0 = blockIdx.x * TW, y0 = blockIdx.y * C::TH_RB;  // x0 is even
     const int R = C::reach(g);
     const bool compress = (C::stride(g) & 1) == 0;
     RbQueue<NT>& q = *reinterpret_cast<RbQueue<NT>*>(smem + rb_queue_offset(tile_bytes(TW, C::TH_RB, R, compress, C::V)));
     if (threadIdx.x == 0) q.next = 0;
-    const Tile t = tile_setup<C>(g, smem, x0, y0, C::TH_RB, compress, (parity + y0) & 1);
+    // the uncompressed window must fit the landing area (TW + 2R) (TH_RB + 2R) float4 <= NT * 8 doubles
+    const bool by_tma = wm.pad >= 0 && compress &&
+                        (size_t)(TW + 2 * R) * (C::TH_RB + 2 * R) * sizeof(float4) <= sizeof(q.costs);
+    const Tile t = by_tma ? tile_setup_tma_compressed<C>(g, wm, smem, reinterpret_cast<float4*>(q.costs), &q.mbar, x0, y0,
+                                                         (parity + y0) & 1)
+                          : tile_setup<C>(g, smem, x0, y0, C::TH_RB, compress, (parity + y0) & 1);
     __syncthreads();
 
     // ---- phase 1
@@ -192,10 +261,12 @@ int fast_red_black(const GroupDev& gd, int parity, const float* di, const float*
                             sizeof(RbQueue<C::NT>);
         if (smem > 200 * 1024) return -1;
         dim3 grid((gd.W + TW - 1) / TW, (gd.H + C::TH_RB - 1) / C::TH_RB);
+        WindowMap wm;
+        make_window_map(gd, g.reach, TW, C::TH_RB, &wm);
         auto k = k_red_black<C>;
         if (prepare(k, smem)) return 1;
         TraceScope ts_("red_black", s);
-        k<<<grid, C::NT, smem, s>>>(g, parity, di, ni, ci, dout, nout, cout, flags_in, flags_out, n_evals);
+        k<<<grid, C::NT, smem, s>>>(g, wm, parity, di, ni, ci, dout, nout, cout, flags_in, flags_out, n_evals);
     })
     return check_launch("red_black_pass");
 }
