@@ -38,9 +38,6 @@ constexpr int TW = 32;  // tile width (pixels)
 #ifndef D360_MINB
 #define D360_MINB 2  // CTAs per SM the register budget is sized for (128 registers)
 #endif
-#ifndef D360_VC_MAX
-#define D360_VC_MAX 4  // views whose projection chains are staged side by side
-#endif
 
 struct FastGroup {
     int W, H, ns, stride, reach, top_k;
@@ -362,104 +359,11 @@ __device__ __forceinline__ double aggregate(double (&cv)[NV], int top_k) {
 
 // NCC sums (K:240-276) of one hypothesis over the views V0 .. V0 + NV - 1 at the pixel whose
 // window entry is `ce`.  `bad` is set when a sample is poisoned (K:242); it does not depend on
-// the views.
-template <class C, typename HT, int V0, int NV>
-__device__ __forceinline__ void accumulate_views(const FastGroup& g, const Tile& t, int ce, double num, HT nx, HT ny,
-                                                 HT nz, bool& bad, double (&s0)[NV], double (&ss0)[NV],
-                                                 double (&rs0)[NV]) {
-#pragma unroll
-    for (int v = 0; v < NV; ++v) s0[v] = ss0[v] = rs0[v] = 0.0;
-    const double2* __restrict__ nb = reinterpret_cast<const double2*>(g.nb64) + (size_t)V0 * g.plane32;
-
-    // lam_k = num / dn_k of sample k (K:240-247) and the f64 luma of that sample
-    auto plane_depth = [&](int es, double& lam, double& rv) {
-        const float4 q = t.qg[es];
-        double dn;
-        if constexpr (sizeof(HT) == 4) {
-            const float den = dot3_f32(nx, ny, nz, q.x, q.y, q.z);
-            bad = bad || (den > g.den_lim);
-            dn = (double)fminf(den, g.den_lim);
-        } else {
-            const double den = fma(nz, (double)q.z, fma(ny, (double)q.y, nx * (double)q.x));
-            const bool par = den > g.neg_par_eps;
-            bad = bad || par;
-            dn = par ? g.neg_par_eps : den;
-        }
-        lam = num * rcp3(dn);
-        rv = (double)q.w;
-    };
-
-    // One flat loop over the S = ns * ns samples (dy outer, dx inner, E:60-65), software-pipelined
-    // by hand: the serial lam chain of sample k+1 (LDS, dot, rcp seed, Newton) is issued next to
-    // the projection chains of sample k instead of in front of them.  (Pipelining the gather of
-    // sample k against the projection of sample k+1 as well was measured: +3 % time, the
-    // 128-register budget has no room for it.)
-    const int ns = C::ns(g);
-    const int half = (ns - 1) / 2;
-    const int n_samples = ns * ns;
-    const int row_wrap = t.sy - ns * t.sx;
-    int e = ce - half * (t.sx + t.sy), col = 0;
-    double lam, rv;
-    plane_depth(e, lam, rv);
-#pragma unroll 1
-    for (int k = 0; k < n_samples; ++k) {
-        int e_next = e + t.sx;
-        if (++col == ns) { col = 0; e_next += row_wrap; }
-        double lam_next = 0.0, rv_next = 0.0;
-        if (k + 1 < n_samples) plane_depth(e_next, lam_next, rv_next);
-        const double* rqe = t.rq + V0 * 3 * t.ne + e;
-        // at most 4 staged chains at a time (more would not fit the register file)
-        constexpr int VC = NV <= D360_VC_MAX ? NV : (NV + 1) / 2;
-#pragma unroll
-        for (int v0 = 0; v0 < NV; v0 += VC) {
-            if (v0 == 0) {
-                double tx[VC], ty[VC], tz[VC], val[VC];
-                float pu[VC], pv[VC];
-#pragma unroll
-                for (int v = 0; v < VC; ++v) {
-                    tx[v] = fma(lam, rqe[(v * 3 + 0) * t.ne], g.rel_t[V0 + v][0]);
-                    ty[v] = fma(lam, rqe[(v * 3 + 1) * t.ne], g.rel_t[V0 + v][1]);
-                    tz[v] = fma(lam, rqe[(v * 3 + 2) * t.ne], g.rel_t[V0 + v][2]);
-                }
-                project_uv<VC>(g, tx, ty, tz, pu, pv);
-                gather_bilinear<VC>(g, nb, g.plane32, pu, pv, val);
-#pragma unroll
-                for (int v = 0; v < VC; ++v) {
-                    s0[v] += val[v];
-                    ss0[v] = fma(val[v], val[v], ss0[v]);
-                    rs0[v] = fma(rv, val[v], rs0[v]);
-                }
-            } else {
-                constexpr int VR = NV - VC > 0 ? NV - VC : 1;  // second (last) chunk
-                double tx[VR], ty[VR], tz[VR], val[VR];
-                float pu[VR], pv[VR];
-#pragma unroll
-                for (int v = 0; v < VR; ++v) {
-                    tx[v] = fma(lam, rqe[((VC + v) * 3 + 0) * t.ne], g.rel_t[V0 + VC + v][0]);
-                    ty[v] = fma(lam, rqe[((VC + v) * 3 + 1) * t.ne], g.rel_t[V0 + VC + v][1]);
-                    tz[v] = fma(lam, rqe[((VC + v) * 3 + 2) * t.ne], g.rel_t[V0 + VC + v][2]);
-                }
-                project_uv<VR>(g, tx, ty, tz, pu, pv);
-                gather_bilinear<VR>(g, nb + (size_t)VC * g.plane32, g.plane32, pu, pv, val);
-#pragma unroll
-                for (int v = 0; v < VR; ++v) {
-                    s0[VC + v] += val[v];
-                    ss0[VC + v] = fma(val[v], val[v], ss0[VC + v]);
-                    rs0[VC + v] = fma(rv, val[v], rs0[VC + v]);
-                }
-            }
-        }
-        e = e_next;
-        lam = lam_next;
-        rv = rv_next;
-    }
-}
-
-// The same sums, SPT samples per trip: consecutive samples are staged side by side, which gives
-// ptxas SPT * NV independent projection chains to interleave (measured at V = 4: -4 % on
-// refine_pass with its three first-pass views, -12 % on its single-view second pass, -2 % on
-// red_black_pass).  The sums take the samples in the same order as accumulate_views, so the
-// results are identical.
+// the views.  One flat loop over the S = ns * ns samples (dy outer, dx inner, E:60-65), SPT
+// samples per trip: consecutive samples are staged side by side, which gives ptxas SPT * NV
+// independent projection chains to interleave (measured at V = 4 against one sample per trip:
+// -4 % on refine_pass with its three first-pass views, -12 % on its single-view second pass,
+// -2 % on red_black_pass).  The sums take the samples in reference order.
 template <class C, typename HT, int V0, int NV, int SPT>
 __device__ __forceinline__ void accumulate_views_multi(const FastGroup& g, const Tile& t, int ce, double num, HT nx,
                                                        HT ny, HT nz, bool& bad, double (&s0)[NV], double (&ss0)[NV],
@@ -577,6 +481,26 @@ __device__ __forceinline__ double view_cost(const FastGroup& g, double s0, doubl
     return c > trunc ? trunc : c;  // NaN (unguarded polar singularities) passes through, see cand_cost
 }
 
+// Per-view costs of views V0 .. V0 + NV - 1 into cv[V0 ...].  Up to four views go through one
+// pass over the samples; more are split into two passes (each repeats the shared plane-depth
+// chain, but keeps its NCC sums and projection chains inside the register budget; V = 6 at
+// 3840x1920: -1 % against one six-view pass).
+template <class C, typename HT, int V0, int NV, int NCV>
+__device__ __forceinline__ void accumulate_costs(const FastGroup& g, const Tile& t, int ce, double num, HT nx, HT ny,
+                                                 HT nz, double mr, double sr, bool& bad, double (&cv)[NCV]) {
+    if constexpr (NV <= 4) {
+        double s0[NV], ss0[NV], rs0[NV];
+        accumulate_views_multi<C, HT, V0, NV, SamplesPerTrip<NV>::value>(g, t, ce, num, nx, ny, nz, bad, s0, ss0, rs0);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) cv[V0 + v] = view_cost(g, s0[v], ss0[v], rs0[v], mr, sr);
+    } else {
+        constexpr int NA = (NV + 1) / 2;
+        accumulate_costs<C, HT, V0, NA>(g, t, ce, num, nx, ny, nz, mr, sr, bad, cv);
+        if (bad) return;
+        accumulate_costs<C, HT, V0 + NA, NV - NA>(g, t, ce, num, nx, ny, nz, mr, sr, bad, cv);
+    }
+}
+
 // Cost of one hypothesis at the pixel whose window entry is `ce` (K:201-297).
 //
 // EARLY (refine_pass): the caller only asks "is the cost below `bound`" (K:600 `ev < c`) and
@@ -608,12 +532,8 @@ __device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, i
     if constexpr (EARLY && VT >= 2) {
         constexpr int VA = VT - 1;
         {
-            double s0[VA], ss0[VA], rs0[VA];
-            if constexpr (VA <= 3) accumulate_views_multi<C, HT, 0, VA, SamplesPerTrip<VA>::value>(g, t, ce, num, nx, ny, nz, bad, s0, ss0, rs0);
-            else accumulate_views<C, HT, 0, VA>(g, t, ce, num, nx, ny, nz, bad, s0, ss0, rs0);
+            accumulate_costs<C, HT, 0, VA>(g, t, ce, num, nx, ny, nz, mr, sr, bad, cv);
             if (bad) return trunc;
-#pragma unroll
-            for (int v = 0; v < VA; ++v) cv[v] = view_cost(g, s0[v], ss0[v], rs0[v], mr, sr);
         }
         {
             double known[VA];
@@ -639,13 +559,8 @@ __device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, i
         }
     } else {
         {
-            double s0[VT], ss0[VT], rs0[VT];
-            if constexpr (VT <= 4) accumulate_views_multi<C, HT, 0, VT, SamplesPerTrip<VT>::value>(g, t, ce, num, nx, ny, nz, bad, s0, ss0, rs0);
-            else
-            accumulate_views<C, HT, 0, VT>(g, t, ce, num, nx, ny, nz, bad, s0, ss0, rs0);
+            accumulate_costs<C, HT, 0, VT>(g, t, ce, num, nx, ny, nz, mr, sr, bad, cv);
             if (bad) return trunc;
-#pragma unroll
-            for (int v = 0; v < VT; ++v) cv[v] = view_cost(g, s0[v], ss0[v], rs0[v], mr, sr);
         }
     }
     const double total = aggregate<VT>(cv, g.top_k);
