@@ -468,7 +468,18 @@ struct SamplesPerTrip {
     static constexpr int value = NV == 1 ? D360_SPT1 : (NV <= 3 ? D360_SPT3 : D360_SPT4);
 };
 
-// K:277-296 for one view: truncated 1 - NCC from the sums
+// 1/sqrt(x), third-order refinement of the MUFU.RSQ64H seed (2^-20 -> ~2^-60)
+__device__ __forceinline__ double rsqrt3(double x, double c0375) {
+    const double y = rsqrt_seed(x);
+    const double e = fma(-(x * y), y, 1.0);
+    return fma(y * e, fma(e, c0375, 0.5), y);
+}
+
+// K:277-296 for one view: truncated 1 - NCC from the sums.  FAST: cov / (sr * sqrt(var)) as
+// cov * rsqrt(var) / sr with the Newton-refined seeds (~1e-18) instead of IEEE sqrt + div, ~15
+// instructions instead of ~70 per view (-1 % on red_black_pass).  refine_pass keeps the IEEE
+// form: there the two extra live values push the sample loop into a register spill (+24 %).
+template <bool FAST>
 __device__ __forceinline__ double view_cost(const FastGroup& g, double s0, double ss0, double rs0, double mr,
                                             double sr) {
     const double trunc = g.trunc, inv_s = g.inv_s;
@@ -476,7 +487,9 @@ __device__ __forceinline__ double view_cost(const FastGroup& g, double s0, doubl
     const double v0 = ss0 * inv_s - m0 * m0;
     if (v0 < D360_VAR_EPS) return trunc;
     const double cov = rs0 * inv_s - mr * m0;
-    double c = 1.0 - cov / (sr * sqrt(v0));
+    double c;
+    if constexpr (FAST) c = fma(-(cov * rcp3(sr)), rsqrt3(v0, g.c0375), 1.0);  // sr >= SIGMA_EPS here
+    else c = 1.0 - cov / (sr * sqrt(v0));
     c = c < 0.0 ? 0.0 : c;
     return c > trunc ? trunc : c;  // NaN (unguarded polar singularities) passes through, see cand_cost
 }
@@ -485,19 +498,19 @@ __device__ __forceinline__ double view_cost(const FastGroup& g, double s0, doubl
 // pass over the samples; more are split into two passes (each repeats the shared plane-depth
 // chain, but keeps its NCC sums and projection chains inside the register budget; V = 6 at
 // 3840x1920: -1 % against one six-view pass).
-template <class C, typename HT, int V0, int NV, int NCV>
+template <class C, typename HT, bool FAST, int V0, int NV, int NCV>
 __device__ __forceinline__ void accumulate_costs(const FastGroup& g, const Tile& t, int ce, double num, HT nx, HT ny,
                                                  HT nz, double mr, double sr, bool& bad, double (&cv)[NCV]) {
     if constexpr (NV <= 4) {
         double s0[NV], ss0[NV], rs0[NV];
         accumulate_views_multi<C, HT, V0, NV, SamplesPerTrip<NV>::value>(g, t, ce, num, nx, ny, nz, bad, s0, ss0, rs0);
 #pragma unroll
-        for (int v = 0; v < NV; ++v) cv[V0 + v] = view_cost(g, s0[v], ss0[v], rs0[v], mr, sr);
+        for (int v = 0; v < NV; ++v) cv[V0 + v] = view_cost<FAST>(g, s0[v], ss0[v], rs0[v], mr, sr);
     } else {
         constexpr int NA = (NV + 1) / 2;
-        accumulate_costs<C, HT, V0, NA>(g, t, ce, num, nx, ny, nz, mr, sr, bad, cv);
+        accumulate_costs<C, HT, FAST, V0, NA>(g, t, ce, num, nx, ny, nz, mr, sr, bad, cv);
         if (bad) return;
-        accumulate_costs<C, HT, V0 + NA, NV - NA>(g, t, ce, num, nx, ny, nz, mr, sr, bad, cv);
+        accumulate_costs<C, HT, FAST, V0 + NA, NV - NA>(g, t, ce, num, nx, ny, nz, mr, sr, bad, cv);
     }
 }
 
@@ -532,7 +545,7 @@ __device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, i
     if constexpr (EARLY && VT >= 2) {
         constexpr int VA = VT - 1;
         {
-            accumulate_costs<C, HT, 0, VA>(g, t, ce, num, nx, ny, nz, mr, sr, bad, cv);
+            accumulate_costs<C, HT, false, 0, VA>(g, t, ce, num, nx, ny, nz, mr, sr, bad, cv);
             if (bad) return trunc;
         }
         {
@@ -555,11 +568,11 @@ __device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, i
             double s0[1], ss0[1], rs0[1];
             bool bad_again = false;  // same samples as the first pass: nothing new
             accumulate_views_multi<C, HT, VA, 1, SamplesPerTrip<1>::value>(g, t, ce, num, nx, ny, nz, bad_again, s0, ss0, rs0);
-            cv[VA] = view_cost(g, s0[0], ss0[0], rs0[0], mr, sr);
+            cv[VA] = view_cost<false>(g, s0[0], ss0[0], rs0[0], mr, sr);
         }
     } else {
         {
-            accumulate_costs<C, HT, 0, VT>(g, t, ce, num, nx, ny, nz, mr, sr, bad, cv);
+            accumulate_costs<C, HT, true, 0, VT>(g, t, ce, num, nx, ny, nz, mr, sr, bad, cv);
             if (bad) return trunc;
         }
     }
