@@ -454,19 +454,9 @@ __device__ __forceinline__ void accumulate_views_multi(const FastGroup& g, const
     }
 }
 
-#ifndef D360_SPT1
-#define D360_SPT1 2  // samples per trip with one view in flight
+#ifndef D360_SPT
+#define D360_SPT 2  // samples per trip (3 and 4 were measured: no further gain, more registers)
 #endif
-#ifndef D360_SPT3
-#define D360_SPT3 2  // ... with two or three views
-#endif
-#ifndef D360_SPT4
-#define D360_SPT4 2  // ... with four views
-#endif
-template <int NV>
-struct SamplesPerTrip {
-    static constexpr int value = NV == 1 ? D360_SPT1 : (NV <= 3 ? D360_SPT3 : D360_SPT4);
-};
 
 // 1/sqrt(x), third-order refinement of the MUFU.RSQ64H seed (2^-20 -> ~2^-60)
 __device__ __forceinline__ double rsqrt3(double x, double c0375) {
@@ -503,7 +493,7 @@ __device__ __forceinline__ void accumulate_costs(const FastGroup& g, const Tile&
                                                  HT nz, double mr, double sr, bool& bad, double (&cv)[NCV]) {
     if constexpr (NV <= 4) {
         double s0[NV], ss0[NV], rs0[NV];
-        accumulate_views_multi<C, HT, V0, NV, SamplesPerTrip<NV>::value>(g, t, ce, num, nx, ny, nz, bad, s0, ss0, rs0);
+        accumulate_views_multi<C, HT, V0, NV, D360_SPT>(g, t, ce, num, nx, ny, nz, bad, s0, ss0, rs0);
 #pragma unroll
         for (int v = 0; v < NV; ++v) cv[V0 + v] = view_cost<FAST>(g, s0[v], ss0[v], rs0[v], mr, sr);
     } else {
@@ -567,7 +557,7 @@ __device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, i
         {
             double s0[1], ss0[1], rs0[1];
             bool bad_again = false;  // same samples as the first pass: nothing new
-            accumulate_views_multi<C, HT, VA, 1, SamplesPerTrip<1>::value>(g, t, ce, num, nx, ny, nz, bad_again, s0, ss0, rs0);
+            accumulate_views_multi<C, HT, VA, 1, D360_SPT>(g, t, ce, num, nx, ny, nz, bad_again, s0, ss0, rs0);
             cv[VA] = view_cost<false>(g, s0[0], ss0[0], rs0[0], mr, sr);
         }
     } else {
