@@ -736,3 +736,30 @@ def test_c4_size_fast_vs_literal_and_fusion(pkg):
     u, v, r = pipeline.project_points(cam, pose0, pts)
     px, py = np.rint(u).astype(int) % cam.width, np.clip(np.rint(v).astype(int), 0, cam.height - 1)
     assert np.abs(r - gt[py, px]).max() < 1e-5
+
+
+@pytest.mark.parametrize("width", [72, 200, 40])
+def test_partial_tiles_fast_vs_literal(pkg, width):
+    """Image sizes that are not multiples of the 32x8 / 32x16 CTA tiles (and, at width 40, barely
+    wider than one tile): the throughput kernels (TMA boxes hanging over the padded plane's edge,
+    partial tiles, wrap inside one tile) against the literal kernels on identical hypotheses."""
+    p, engine, _, synth = pkg
+    cam = p.EquirectCamera(width, width // 2)
+    group, _ = synth.make_group(synth.default_scene("box"), cam, n_views=4)
+    spec, dr = engine.PatchSpec(), (0.5, 16.0)
+    out = {}
+    for prec in ("mixed", "exact"):
+        prep = engine.prepare_group(group, spec, precision=prec)
+        pm = engine.DevicePlaneMap.empty(cam, dr)
+        engine.random_init_device(pm, dr, 1, "philox")
+        engine.evaluate_costs_device(prep, pm)
+        c0 = pm.cost.clone()
+        nxt = pm.clone()
+        engine.red_black_pass_device(prep, 1, pm, nxt)
+        tab = engine.refinement_draw_tables(1, 1, 0.25 * (dr[1] - dr[0]), np.radians(60.0))[0]
+        engine.refine_pass_device(prep, nxt, tab, dr)
+        out[prec] = (c0.cpu().numpy(), nxt.depth.cpu().numpy(), nxt.cost.cpu().numpy())
+    assert cost_close(out["mixed"][0], out["exact"][0]).all()
+    same = out["mixed"][1] == out["exact"][1]
+    assert same.mean() >= 0.995
+    assert cost_close(out["mixed"][2][same], out["exact"][2][same]).all()
