@@ -157,26 +157,35 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
         // duplicate, so comparing with the pixel's original hypothesis and with the earlier
         // neighbours selects the same set, except that it also skips re-evaluating the original
         // hypothesis once it has been displaced, which strict < would reject anyway.
+        //
+        // The eight neighbour hypotheses are fetched first, as 40 independent loads, and compared
+        // in registers: this phase is pure memory latency and sits in front of every CTA's work
+        // (a loop of dependent loads here cost ~0.3 ms per launch, 7 % of a step).
+        constexpr int NDX[8] = {-1, 1, -1, 1, 0, 0, -2, 2}, NDY[8] = {-1, -1, 1, 1, -2, 2, 0, 0};
+        float hd[8], hx[8], hy[8], hz[8];
+        unsigned char changed[8];
+        bool in_range[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int qy = y + NDY[j];
+            in_range[j] = qy >= 0 && qy < g.H;                                          // K:407 rows skipped
+            const size_t qi = in_range[j] ? (size_t)qy * g.W + wrap_once(x + NDX[j], g.W) : i;  // K:410-413 columns wrap
+            hd[j] = depth_in[qi];
+            hx[j] = normal_in[3 * qi];
+            hy[j] = normal_in[3 * qi + 1];
+            hz[j] = normal_in[3 * qi + 2];
+            changed[j] = flags_in != nullptr ? flags_in[qi] : (unsigned char)1;
+        }
         const bool may_skip = flags_in != nullptr && flags_in[i] == 0;
         const float od = depth_in[i];
         const float onx = normal_in[3 * i], ony = normal_in[3 * i + 1], onz = normal_in[3 * i + 2];
-#pragma unroll 1
+#pragma unroll
         for (int j = 0; j < 8; ++j) {
-            const int qy = y + c_nbr2[j][1];
-            if (qy < 0 || qy >= g.H) continue;  // K:407 rows skipped
-            const size_t qi = (size_t)qy * g.W + wrap_once(x + c_nbr2[j][0], g.W);  // K:410-413 columns wrap
-            const float d = depth_in[qi];
-            const float nx = normal_in[3 * qi], ny = normal_in[3 * qi + 1], nz = normal_in[3 * qi + 2];
-            bool dup = d == od && nx == onx && ny == ony && nz == onz;
-            for (int m = 0; m < j; ++m) {
-                const int my = y + c_nbr2[m][1];
-                if (my < 0 || my >= g.H) continue;
-                const size_t mi = (size_t)my * g.W + wrap_once(x + c_nbr2[m][0], g.W);
-                if (depth_in[mi] == d)
-                    dup = dup || (normal_in[3 * mi] == nx && normal_in[3 * mi + 1] == ny &&
-                                  normal_in[3 * mi + 2] == nz);
-            }
-            if (!dup && (!may_skip || flags_in[qi])) mask |= 1u << j;
+            bool dup = hd[j] == od && hx[j] == onx && hy[j] == ony && hz[j] == onz;
+#pragma unroll
+            for (int m = 0; m < j; ++m)
+                dup = dup || (in_range[m] && hd[m] == hd[j] && hx[m] == hx[j] && hy[m] == hy[j] && hz[m] == hz[j]);
+            if (in_range[j] && !dup && (!may_skip || changed[j])) mask |= 1u << j;
         }
     }
     const int n_mine = __popc(mask);
