@@ -4,7 +4,8 @@
 // a pixel has to evaluate varies (0..8 after the duplicate skipping of K:418-432), so the work
 // is levelled through a CTA-wide queue:
 //   phase 1  one thread per pixel: in-range, non-duplicate neighbours -> candidate mask;
-//            patch statistics; exclusive scan of the counts; (pixel, neighbour) items queued;
+//            exclusive scan of the counts; (pixel, neighbour) items queued.  The patch window
+//            is being loaded meanwhile and is only unpacked if the CTA has any item at all;
 //   phase 2  warps pull 32 items at a time and evaluate them (any lane, any pixel of the tile);
 //   phase 3  one thread per pixel: strict-< arg-min over its candidates in neighbour order
 //            (K:463; the cost of a hypothesis does not depend on evaluation order, so this is
@@ -48,42 +49,47 @@ __host__ __device__ inline size_t rb_queue_offset(size_t tile) { return (tile + 
 
 // Colour-compressed window from one TMA box: the full (TW + 2R) x (TH_RB + 2R) float4 window lands
 // in `stage` (the queue's cost array, not needed before phase 2), then every thread copies the
-// entries of the pass's colour to their compressed slots and derives R_v q for them.
+// entries of the pass's colour to their compressed slots and derives R_v q for them.  Issue and
+// completion are separate so that the load is in flight during phase 1.
 template <class C>
-__device__ __forceinline__ Tile tile_setup_tma_compressed(const FastGroup& g, const WindowMap& wm, unsigned char* smem,
-                                                          float4* stage, unsigned long long* mbar, int x0, int y0,
-                                                          int keep) {
+__device__ __forceinline__ void window_tma_issue(const FastGroup& g, const WindowMap& wm, float4* stage,
+                                                 unsigned long long* mbar, int x0, int y0) {
+    const int R = C::reach(g);
+    const int ww = TW + 2 * R, hh = C::TH_RB + 2 * R;
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)),
+                 "r"((unsigned)(ww * hh * sizeof(float4)))
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(stage)),
+        "l"(reinterpret_cast<unsigned long long>(&wm.map)), "r"(4 * (x0 - R + wm.pad)), "r"(y0 - R + wm.pad),
+        "r"(smem_u32(mbar))
+        : "memory");
+}
+
+__device__ __forceinline__ void window_tma_wait(unsigned long long* mbar) {
+    unsigned done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(mbar))
+            : "memory");
+    }
+}
+
+template <class C>
+__device__ __forceinline__ Tile window_from_stage(const FastGroup& g, unsigned char* smem, const float4* stage,
+                                                  int keep) {
     const int R = C::reach(g);
     const int ww = TW + 2 * R, hh = C::TH_RB + 2 * R;
     const int wwc = ww / 2;
     const int ne = wwc * hh;
     float4* qg = reinterpret_cast<float4*>(smem);
     double* rq = reinterpret_cast<double*>(smem + (size_t)ne * sizeof(float4));
-    if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)));
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)),
-                     "r"((unsigned)(ww * hh * sizeof(float4)))
-                     : "memory");
-        asm volatile(
-            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-                smem_u32(stage)),
-            "l"(reinterpret_cast<unsigned long long>(&wm.map)), "r"(4 * (x0 - R + wm.pad)), "r"(y0 - R + wm.pad),
-            "r"(smem_u32(mbar))
-            : "memory");
-    }
-    __syncthreads();
-    {
-        unsigned done = 0;
-        while (!done) {
-            asm volatile(
-                "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-                : "=r"(done)
-                : "r"(smem_u32(mbar))
-                : "memory");
-        }
-    }
     for (int e = threadIdx.x; e < ne; e += C::NT) {
         const int j = e / wwc, ic = e - j * wwc;
         const int i = 2 * ic + ((keep + j) & 1);
@@ -125,10 +131,8 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
     // the uncompressed window must fit the landing area (TW + 2R) (TH_RB + 2R) float4 <= NT * 8 doubles
     const bool by_tma = wm.pad >= 0 && compress &&
                         (size_t)(TW + 2 * R) * (C::TH_RB + 2 * R) * sizeof(float4) <= sizeof(q.costs);
-    const Tile t = by_tma ? tile_setup_tma_compressed<C>(g, wm, smem, reinterpret_cast<float4*>(q.costs), &q.mbar, x0, y0,
-                                                         (parity + y0) & 1)
-                          : tile_setup<C>(g, smem, x0, y0, C::TH_RB, compress, (parity + y0) & 1);
-    __syncthreads();
+    if (by_tma && threadIdx.x == 0) window_tma_issue<C>(g, wm, reinterpret_cast<float4*>(q.costs), &q.mbar, x0, y0);
+    __syncthreads();  // queue head and barrier initialised; the window load is in flight during phase 1
 
     // ---- phase 1
     const int tid = threadIdx.x;
@@ -189,12 +193,6 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
         }
     }
     const int n_mine = __popc(mask);
-    if (n_mine) {
-        const int ce = (ly + R) * t.wwc + (compress ? (lx + R) >> 1 : lx + R);
-        double mr, sr;
-        pixel_stats<C>(g, t, ce, mr, sr);
-        q.stats[tid] = make_double2(mr, sr);
-    }
     int incl = n_mine;  // CTA-wide exclusive scan of the counts
     for (int o = 1; o < 32; o <<= 1) {
         const int up = __shfl_up_sync(0xffffffffu, incl, o);
@@ -207,30 +205,43 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
     if (tid == NT - 1) q.total = off + n_mine;
     for (unsigned m = mask; m; m &= m - 1) q.items[off++] = (unsigned short)(tid * 8 + (__ffs(m) - 1));
     __syncthreads();
-
-    // ---- phase 2
     const int total = q.total;
-    for (;;) {
-        int base = 0;
-        if ((tid & 31) == 0) base = atomicAdd(&q.next, 32);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (base >= total) break;
-        const int it = base + (tid & 31);
-        if (it < total) {
-            const int item = q.items[it];
-            const int p = item >> 3, j = item & 7;
-            const int ply = p / (TW / 2);
-            const int py = y0 + ply;
-            const int plx = 2 * (p % (TW / 2)) + ((parity + py) & 1);
-            const int px = x0 + plx;
-            const size_t qi = (size_t)(py + c_nbr2[j][1]) * g.W + wrap_once(px + c_nbr2[j][0], g.W);
-            const int ce = (ply + R) * t.wwc + (compress ? (plx + R) >> 1 : plx + R);
-            const double2 st = q.stats[p];
-            q.costs[item] = cand_cost<C, float>(g, t, ce, st.x, st.y, depth_in[qi], normal_in[3 * qi],
-                                                normal_in[3 * qi + 1], normal_in[3 * qi + 2]);
+    if (by_tma) window_tma_wait(&q.mbar);  // also with nothing to do: never leave with a copy in flight
+
+    // ---- phase 2 (skipped, with the whole patch window, by a CTA that has no candidate left)
+    if (total > 0) {
+        const Tile t = by_tma ? window_from_stage<C>(g, smem, reinterpret_cast<const float4*>(q.costs), (parity + y0) & 1)
+                              : tile_setup<C>(g, smem, x0, y0, C::TH_RB, compress, (parity + y0) & 1);
+        __syncthreads();
+        if (n_mine) {
+            const int ce = (ly + R) * t.wwc + (compress ? (lx + R) >> 1 : lx + R);
+            double mr, sr;
+            pixel_stats<C>(g, t, ce, mr, sr);
+            q.stats[tid] = make_double2(mr, sr);
         }
+        __syncthreads();
+        for (;;) {
+            int base = 0;
+            if ((tid & 31) == 0) base = atomicAdd(&q.next, 32);
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (base >= total) break;
+            const int it = base + (tid & 31);
+            if (it < total) {
+                const int item = q.items[it];
+                const int p = item >> 3, j = item & 7;
+                const int ply = p / (TW / 2);
+                const int py = y0 + ply;
+                const int plx = 2 * (p % (TW / 2)) + ((parity + py) & 1);
+                const int px = x0 + plx;
+                const size_t qi = (size_t)(py + c_nbr2[j][1]) * g.W + wrap_once(px + c_nbr2[j][0], g.W);
+                const int ce = (ply + R) * t.wwc + (compress ? (plx + R) >> 1 : plx + R);
+                const double2 st = q.stats[p];
+                q.costs[item] = cand_cost<C, float>(g, t, ce, st.x, st.y, depth_in[qi], normal_in[3 * qi],
+                                                    normal_in[3 * qi + 1], normal_in[3 * qi + 2]);
+            }
+        }
+        __syncthreads();
     }
-    __syncthreads();
 
     // ---- phase 3
     if (live) {
