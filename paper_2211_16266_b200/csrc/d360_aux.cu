@@ -259,25 +259,55 @@ __global__ void __launch_bounds__(MED_TW* MED_TH)
     const int win = 2 * half + 1;
     // a window wider than the image would revisit columns; the reference does the same
     int n = 0;
-    for (int j = 0; j < win; ++j)
-        for (int i = 0; i < win; ++i) n += !isnan(tile[(ly + j) * ww + lx + i]);
-    const int k_hi = n / 2, k_lo = (n % 2 == 1) ? n / 2 : n / 2 - 1;
     float v_hi = 0.0f, v_lo = 0.0f;
-    for (int j = 0; j < win; ++j)
-        for (int i = 0; i < win; ++i) {
-            const int ei = (ly + j) * ww + lx + i;
-            const float vi = tile[ei];
-            if (isnan(vi)) continue;
-            int rank = 0;  // elements strictly smaller, ties broken by window position
-            for (int jj = 0; jj < win; ++jj)
-                for (int ii = 0; ii < win; ++ii) {
-                    const int ej = (ly + jj) * ww + lx + ii;
-                    const float vj = tile[ej];
-                    rank += (vj < vi) || (vj == vi && ej < ei);
-                }
-            if (rank == k_hi) v_hi = vi;
-            if (rank == k_lo) v_lo = vi;
+    if (half == 2) {
+        // the default 5x5 window: 25 values in registers (invalid -> +inf, sorted last), odd-even
+        // transposition network, then the two middle ranks of the n valid ones picked by position
+        float w[25];
+        const float inf = __int_as_float(0x7f800000);
+#pragma unroll
+        for (int j = 0; j < 5; ++j)
+#pragma unroll
+            for (int i = 0; i < 5; ++i) {
+                const float v = tile[(ly + j) * ww + lx + i];
+                const bool ok = !isnan(v);
+                n += ok;
+                w[j * 5 + i] = ok ? v : inf;
+            }
+#pragma unroll
+        for (int round = 0; round < 25; ++round)
+#pragma unroll
+            for (int a = round & 1; a + 1 < 25; a += 2) {
+                const float lo = fminf(w[a], w[a + 1]), hi = fmaxf(w[a], w[a + 1]);
+                w[a] = lo;
+                w[a + 1] = hi;
+            }
+        const int k_hi = n / 2, k_lo = (n % 2 == 1) ? n / 2 : n / 2 - 1;
+#pragma unroll
+        for (int a = 0; a < 25; ++a) {
+            v_hi = a == k_hi ? w[a] : v_hi;
+            v_lo = a == k_lo ? w[a] : v_lo;
         }
+    } else {
+        for (int j = 0; j < win; ++j)
+            for (int i = 0; i < win; ++i) n += !isnan(tile[(ly + j) * ww + lx + i]);
+        const int k_hi = n / 2, k_lo = (n % 2 == 1) ? n / 2 : n / 2 - 1;
+        for (int j = 0; j < win; ++j)
+            for (int i = 0; i < win; ++i) {
+                const int ei = (ly + j) * ww + lx + i;
+                const float vi = tile[ei];
+                if (isnan(vi)) continue;
+                int rank = 0;  // elements strictly smaller, ties broken by window position
+                for (int jj = 0; jj < win; ++jj)
+                    for (int ii = 0; ii < win; ++ii) {
+                        const int ej = (ly + jj) * ww + lx + ii;
+                        const float vj = tile[ej];
+                        rank += (vj < vi) || (vj == vi && ej < ei);
+                    }
+                if (rank == k_hi) v_hi = vi;
+                if (rank == k_lo) v_lo = vi;
+            }
+    }
     const double med = (n % 2 == 1) ? (double)v_hi : 0.5 * (double)__fadd_rn(v_lo, v_hi);
     out_valid[gi] = fabs((double)depth[gi] - med) <= rel_threshold * med;
 }
