@@ -74,6 +74,15 @@ def sequence_positions(rank: int):
     return [np.array([x, y, z0 + k * STEP_M]) for k in range(SEQ_LEN)]
 
 
+def loop_positions(rank: int):
+    """The line of sequence_positions followed by a second lane, one step to the side, walked back:
+    a closed loop of 2 SEQ_LEN distinct keyframes with STEP_M between any two consecutive ones, so a
+    stream of any length never meets the same position twice inside one stereo window."""
+    lane_a = sequence_positions(rank)
+    lane_b = [t + np.array([STEP_M, 0.0, 0.0]) for t in reversed(lane_a)]
+    return lane_a + lane_b
+
+
 def walk(n: int):
     """Indices 2..SEQ_LEN-3 walked back and forth, so every group has its 4 neighbours."""
     lo, hi = 2, SEQ_LEN - 3
@@ -249,9 +258,16 @@ def run_product(args) -> dict | None:
                                          init_rng="philox", device=dev)
     fill = V + ccfg.window - 1  # pushes before the first output
     n_push = fill + args.warmup + args.steps
-    fwd = list(range(SEQ_LEN))
-    cyc = fwd + fwd[-2:0:-1]
-    positions = [cyc[k % len(cyc)] for k in range(n_push)]
+    if n_push > SEQ_LEN:  # longer than the line: continue around the two-lane loop (second lane rendered here)
+        for t in loop_positions(rank)[SEQ_LEN:]:
+            pose = p.RigidPose(np.eye(3), t)
+            img, _ = synth.render_scene_device(scene, cam, pose, dev)
+            pinned = torch.empty(img.shape, dtype=torch.uint8).pin_memory()
+            pinned.copy_(img)
+            poses.append(pose)
+            host_imgs.append(pinned.numpy())
+        torch.cuda.synchronize()
+    positions = [k % len(poses) for k in range(n_push)]
     bytes_in = bytes_out = 0
     produced = 0
 
