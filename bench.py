@@ -23,6 +23,7 @@ except for the `cpu_baseline` leg at N=1.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
@@ -237,14 +238,24 @@ def run_product(args) -> dict | None:
     _lib.trace_enable(True)
     launches0 = _lib.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    gc.collect()
+    gc.disable()
     with ClockSampler(local_rank) as clocks:
         barrier()
         e0.record()
+        marks = []
         for i in order[args.warmup:]:
             step_device(i)
+            if os.environ.get("D360_BENCH_DEBUG"):
+                marks.append(torch.cuda.Event(enable_timing=True))
+                marks[-1].record()
         e1.record()
         barrier()
+    gc.enable()
     dev_ms = e0.elapsed_time(e1)
+    if marks:
+        print("device per-step gpu ms:", [round(a.elapsed_time(b), 1) for a, b in zip([e0] + marks[:-1], marks)],
+              file=sys.stderr)
     launches = _lib.launch_count() - launches0
     trace = _lib.trace_summary()
     _lib.trace_enable(False)
@@ -284,12 +295,28 @@ def run_product(args) -> dict | None:
     for k in range(fill + args.warmup):
         step_host(k)
     bytes_in = bytes_out = produced = 0
+    per_step, evs = [], []
+    debug = bool(os.environ.get("D360_BENCH_DEBUG"))
+    gc.collect()
+    gc.disable()  # keep the cyclic collector out of the 0.5 s timed region
     barrier()
     t0 = time.perf_counter()
     for k in range(fill + args.warmup, n_push):
+        ts = time.perf_counter()
+        if debug:
+            ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ea.record()
         step_host(k)
+        if debug:
+            eb.record()
+            evs.append((ea, eb))
+        per_step.append(time.perf_counter() - ts)
     barrier()
     e2e_s = time.perf_counter() - t0
+    gc.enable()
+    if debug:
+        print("e2e per-step wall ms:", [round(x * 1e3, 1) for x in per_step], file=sys.stderr)
+        print("e2e per-step gpu  ms:", [round(a.elapsed_time(b), 1) for a, b in evs], file=sys.stderr)
     if produced != args.steps:
         raise SystemExit(f"streaming leg produced {produced} depth maps in {args.steps} steps")
 

@@ -116,11 +116,12 @@ int d360_refine_pass(const d360_group *g, float *depth, float *normal, float *co
  * x (red, black, refine) with state resident on the device.  tables: host
  * (iterations,5,n_cand) f32 in the order (dd, sin ang, cos ang, cos az, sin az).
  * depth/normal in/out, cost out; scratch_* are caller-owned ping-pong buffers of the same
- * shapes.  scratch_changed (optional, u8, 2*H*W bytes): work area for unchanged-neighbour
- * skipping — a pixel that did not change during the previous iteration does not re-test the
- * hypothesis of a neighbour that did not change either (the re-test is certainly rejected
- * again, K:463 is strict <); results are bit-identical with and without it, only fewer
- * evaluations run (csrc/d360_fast_rb.cu).
+ * shapes.  scratch_flags (u8, 3*H*W bytes) and scratch_memo (f64, 8*H*W) — optional, both or
+ * neither — are the work area of memoised candidate costs: the cost of a neighbour's
+ * hypothesis at a pixel is a pure function of the two, so a propagation pass re-evaluates a
+ * candidate only when that neighbour's hypothesis changed since the pixel last evaluated it
+ * and otherwise reuses the f64 cost it computed then; results are bit-identical with and
+ * without it, only fewer evaluations run (csrc/d360_fast_rb.cu).
  * valid_out (optional, u8) = cost < trunc (E:629).
  * n_evals (device, optional, uint64[2]): [0] += cost evaluations started (propagation +
  * refinement), [1] += refinement evaluations that were decided after V - 1 views (the last
@@ -128,8 +129,8 @@ int d360_refine_pass(const d360_group *g, float *depth, float *normal, float *co
  * and so did 1/V less work. */
 int d360_run_patchmatch(const d360_group *g, float *depth, float *normal, float *cost,
                         float *scratch_depth, float *scratch_normal, float *scratch_cost,
-                        uint8_t *scratch_changed, const float *tables, int iterations, int n_cand,
-                        double depth_min,
+                        uint8_t *scratch_flags, double *scratch_memo, const float *tables,
+                        int iterations, int n_cand, double depth_min,
                         double depth_max, uint8_t *valid_out, unsigned long long *n_evals,
                         void *stream);
 

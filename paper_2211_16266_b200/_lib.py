@@ -50,7 +50,7 @@ _SIGNATURES = {
     "d360_eval_costs": (C.c_int, [C.POINTER(Group), c_void, c_void, c_void, c_void]),
     "d360_red_black_pass": (C.c_int, [C.POINTER(Group), C.c_int] + [c_void] * 8),
     "d360_refine_pass": (C.c_int, [C.POINTER(Group)] + [c_void] * 8 + [C.c_int, C.c_double, C.c_double, c_void]),
-    "d360_run_patchmatch": (C.c_int, [C.POINTER(Group)] + [c_void] * 8 + [C.c_int, C.c_int, C.c_double,
+    "d360_run_patchmatch": (C.c_int, [C.POINTER(Group)] + [c_void] * 9 + [C.c_int, C.c_int, C.c_double,
                                                                          C.c_double, c_void, c_void, c_void]),
     "d360_build_ref_context": (C.c_int, [c_void, c_void, c_void, C.c_int, C.c_int, C.c_int, c_void]),
     "d360_median_support_mask": (C.c_int, [c_void, c_void, C.c_int, C.c_double, c_void, C.c_int, C.c_int, c_void]),

@@ -63,7 +63,8 @@ struct RefineTable {
 int fast_eval(const struct GroupDev& gd, const float* depth, const float* normal, float* cost_out, cudaStream_t s);
 int fast_red_black(const struct GroupDev& gd, int parity, const float* di, const float* ni, const float* ci,
                    float* dout, float* nout, float* cout, const unsigned char* changed_in,
-                   unsigned char* changed_out, unsigned long long* n_evals, cudaStream_t s);
+                   unsigned char* changed_out, unsigned char* memo_valid, double* memo_cost,
+                   unsigned long long* n_evals, cudaStream_t s);
 int fast_refine(const struct GroupDev& gd, const RefineTable& tab, float* depth, float* normal, float* cost,
                 unsigned char* changed, unsigned long long* n_evals, cudaStream_t s);
 

@@ -11,22 +11,21 @@
 //            (K:463; the cost of a hypothesis does not depend on evaluation order, so this is
 //            the reference's sequential accept).
 //
-// Unchanged-neighbour skipping (optional, `flags_in` / `flags_out`, one byte per pixel): a pixel p
-// that has itself not changed since its previous pass need not re-test the hypothesis of a
-// neighbour q that has not changed either.  The cost of a hypothesis at a pixel is a pure
-// function and acceptance is strict <: in the previous pass q's hypothesis was either evaluated
-// and not better than p's cost — which is still the same f32 value — or skipped as a duplicate
-// of p's own, still identical, hypothesis (K:418-432), or skipped by this rule, and then the
-// argument recurses.  The results are bit-identical; only evaluations are saved.  (p itself
-// must be unchanged: after a refinement accept the stored f32 hypothesis is not the f64 one its
-// stored cost was computed from, so "duplicate of my own hypothesis" no longer implies "not
-// better than my cost" once p moves on; and a cost that was stored after rounding up lets the
-// reference accept an equal-cost candidate, e.g. at the truncation cost, f32(1.2) > 1.2.)
-//   flag = 1: the pixel's hypothesis changed during its own red-black pass or the refinement
+// Memoised candidate costs (optional: `flags_in` / `flags_out`, `memo_valid`, `memo_cost`).  The
+// cost of hypothesis h at pixel p is a pure function of (p, h) — p's own hypothesis does not
+// enter it — so c_p(h_q) stays what it was for as long as the neighbour q keeps its hypothesis.
+// Per pixel the pass keeps the eight costs it last computed (f64, exactly the values phase 2
+// produced) and a validity byte; at the next pass it drops the entries of neighbours whose
+// "changed" flag is set, evaluates only the in-range, non-duplicate candidates without a valid
+// entry, and takes the arg-min over fresh and remembered costs alike.  Duplicates (K:418-432)
+// stay excluded exactly as before, so the result is bit-identical to evaluating everything; on a
+// warp-initialised sequence 40-45 % of the propagation evaluations of the later iterations are
+// remembered ones.
+//   flags: 1 = the pixel's hypothesis changed during its own red-black pass or the refinement
 //   of the previous iteration.  The first iteration starts from all ones.  A pass writes
 //   flags_out for the pixels it updates and refine_pass sets it where it accepts.  All eight
 //   neighbours have the pixel's colour, so a pass reads only flags that no pass of the same
-//   iteration writes.
+//   iteration writes, and only pixel p touches p's memo entries.
 #include "d360_fast.cuh"
 
 namespace d360 {
@@ -120,7 +119,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
                 const float* __restrict__ normal_in, const float* __restrict__ cost_in, float* __restrict__ depth_out,
                 float* __restrict__ normal_out, float* __restrict__ cost_out,
                 const unsigned char* __restrict__ flags_in, unsigned char* __restrict__ flags_out,
-                unsigned long long* n_evals) {
+                unsigned char* __restrict__ memo_valid, double* __restrict__ memo_cost, unsigned long long* n_evals) {
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr int NT = C::NT;
     const int x0 = blockIdx.x * TW, y0 = blockIdx.y * C::TH_RB;  // x0 is even
@@ -154,7 +153,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
         }
     }
     const size_t i = live ? (size_t)y * g.W + x : 0;
-    unsigned mask = 0;
+    unsigned mask = 0, considered = 0, kept = 0;  // to evaluate now; all candidates of the arg-min; valid memo entries
     if (live) {
         // K:418-432 skips exact duplicates of the best-so-far and of already evaluated
         // candidates.  Every earlier in-range neighbour was either evaluated or itself such a
@@ -180,17 +179,20 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
             hz[j] = normal_in[3 * qi + 2];
             changed[j] = flags_in != nullptr ? flags_in[qi] : (unsigned char)1;
         }
-        const bool may_skip = flags_in != nullptr && flags_in[i] == 0;
         const float od = depth_in[i];
         const float onx = normal_in[3 * i], ony = normal_in[3 * i + 1], onz = normal_in[3 * i + 2];
+        unsigned remembered = memo_valid != nullptr && flags_in != nullptr ? memo_valid[i] : 0u;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             bool dup = hd[j] == od && hx[j] == onx && hy[j] == ony && hz[j] == onz;
 #pragma unroll
             for (int m = 0; m < j; ++m)
                 dup = dup || (in_range[m] && hd[m] == hd[j] && hx[m] == hx[j] && hy[m] == hy[j] && hz[m] == hz[j]);
-            if (in_range[j] && !dup && (!may_skip || changed[j])) mask |= 1u << j;
+            if (in_range[j] && !dup) considered |= 1u << j;
+            if (changed[j]) remembered &= ~(1u << j);
         }
+        kept = remembered;
+        mask = considered & ~remembered;
     }
     const int n_mine = __popc(mask);
     int incl = n_mine;  // CTA-wide exclusive scan of the counts
@@ -247,9 +249,15 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
     if (live) {
         double bc = (double)cost_in[i];
         int bj = -1;
-        for (unsigned m = mask; m; m &= m - 1) {
+        for (unsigned m = considered; m; m &= m - 1) {
             const int j = __ffs(m) - 1;
-            const double c = q.costs[tid * 8 + j];
+            double c;
+            if (mask >> j & 1u) {
+                c = q.costs[tid * 8 + j];
+                if (memo_cost != nullptr) __stcs(memo_cost + 8 * i + j, c);
+            } else {
+                c = __ldcs(memo_cost + 8 * i + j);  // computed by an earlier pass for the same (pixel, hypothesis)
+            }
             if (c < bc) {  // K:463
                 bc = c;
                 bj = j;
@@ -263,6 +271,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
         normal_out[3 * i + 2] = normal_in[3 * bi + 2];
         cost_out[i] = (float)bc;
         if (flags_out != nullptr) flags_out[i] = bj >= 0;
+        if (memo_valid != nullptr) memo_valid[i] = (unsigned char)(kept | mask);
     }
     if (n_evals != nullptr && tid == 0 && total) atomicAdd(n_evals, (unsigned long long)total);
 }
@@ -273,7 +282,7 @@ using namespace fast;
 
 int fast_red_black(const GroupDev& gd, int parity, const float* di, const float* ni, const float* ci, float* dout,
                    float* nout, float* cout, const unsigned char* flags_in, unsigned char* flags_out,
-                   unsigned long long* n_evals, cudaStream_t s) {
+                   unsigned char* memo_valid, double* memo_cost, unsigned long long* n_evals, cudaStream_t s) {
     FastGroup g;
     if (!make_fast_group(gd, &g)) return -1;
     D360_FAST_DISPATCH(gd.V, {
@@ -286,7 +295,7 @@ int fast_red_black(const GroupDev& gd, int parity, const float* di, const float*
         auto k = k_red_black<C>;
         if (prepare(k, smem)) return 1;
         TraceScope ts_("red_black", s);
-        k<<<grid, C::NT, smem, s>>>(g, wm, parity, di, ni, ci, dout, nout, cout, flags_in, flags_out, n_evals);
+        k<<<grid, C::NT, smem, s>>>(g, wm, parity, di, ni, ci, dout, nout, cout, flags_in, flags_out, memo_valid, memo_cost, n_evals);
     })
     return check_launch("red_black_pass");
 }

@@ -459,16 +459,22 @@ static int launch_eval(const GroupDev& gd, int prec, const float* depth, const f
     return rc ? rc : check_launch("eval_costs");
 }
 
-// changed_in / changed_out (optional): unchanged-neighbour skipping of the throughput kernels
-// (d360_fast_rb.cu).  The generic kernels do not use the flags; they mark every pixel changed,
-// which is always safe.
+// changed_in / changed_out, memo_valid / memo_cost (optional): memoised candidate costs of the
+// throughput kernels (d360_fast_rb.cu).  The generic kernels do not use them; they mark every
+// pixel changed and drop every memo entry, which is always safe.
 static int launch_red_black(const GroupDev& gd, int prec, int parity, const float* di,
                             const float* ni, const float* ci, float* dout, float* nout, float* cout,
                             const unsigned char* changed_in, unsigned char* changed_out,
-                            unsigned long long* n_evals, cudaStream_t s) {
+                            unsigned char* memo_valid, double* memo_cost, unsigned long long* n_evals,
+                            cudaStream_t s) {
     if (prec == D360_PREC_MIXED) {
-        const int frc = fast_red_black(gd, parity, di, ni, ci, dout, nout, cout, changed_in, changed_out, n_evals, s);
+        const int frc = fast_red_black(gd, parity, di, ni, ci, dout, nout, cout, changed_in, changed_out, memo_valid,
+                                       memo_cost, n_evals, s);
         if (frc >= 0) return frc;
+    }
+    if (memo_valid != nullptr && cudaMemsetAsync(memo_valid, 0, (size_t)gd.W * gd.H, s) != cudaSuccess) {
+        set_error("cudaMemsetAsync(memo validity) failed");
+        return 1;
     }
     if (changed_out != nullptr && cudaMemsetAsync(changed_out, 1, (size_t)gd.W * gd.H, s) != cudaSuccess) {
         set_error("cudaMemsetAsync(changed flags) failed");
@@ -558,7 +564,7 @@ extern "C" int d360_red_black_pass(const d360_group* g, int parity, const float*
         return 1;
     }
     return launch_red_black(gd, g->precision, parity, depth_in, normal_in, cost_in, depth_out,
-                            normal_out, cost_out, nullptr, nullptr, n_evals, (cudaStream_t)stream);
+                            normal_out, cost_out, nullptr, nullptr, nullptr, nullptr, n_evals, (cudaStream_t)stream);
 }
 
 extern "C" int d360_refine_pass(const d360_group* g, float* depth, float* normal, float* cost,
@@ -575,8 +581,8 @@ extern "C" int d360_refine_pass(const d360_group* g, float* depth, float* normal
 
 extern "C" int d360_run_patchmatch(const d360_group* g, float* depth, float* normal, float* cost,
                                    float* scratch_depth, float* scratch_normal, float* scratch_cost,
-                                   uint8_t* scratch_changed, const float* tables, int iterations, int n_cand,
-                                   double depth_min,
+                                   uint8_t* scratch_flags, double* scratch_memo, const float* tables, int iterations,
+                                   int n_cand, double depth_min,
                                    double depth_max, uint8_t* valid_out, unsigned long long* n_evals,
                                    void* stream) {
     GroupDev gd;
@@ -590,17 +596,23 @@ extern "C" int d360_run_patchmatch(const d360_group* g, float* depth, float* nor
     if (launch_eval(gd, prec, depth, normal, cost, s)) return 1;
     float *cd = depth, *cn = normal, *cc = cost;
     float *nd = scratch_depth, *nn = scratch_normal, *nc = scratch_cost;
-    // unchanged-neighbour skipping: two flag planes, read one / write the other, swapped per iteration
+    // memoised candidate costs: two "changed" flag planes (read one / write the other, swapped per
+    // iteration), one validity plane, eight f64 costs per pixel
     const size_t n_px = (size_t)gd.W * gd.H;
-    unsigned char* chg_in = scratch_changed;
-    unsigned char* chg_out = scratch_changed != nullptr ? scratch_changed + n_px : nullptr;
-    if (chg_in != nullptr && cudaMemsetAsync(chg_in, 1, n_px, s) != cudaSuccess) {
-        set_error("cudaMemsetAsync(changed flags) failed");
+    const bool memo = scratch_flags != nullptr && scratch_memo != nullptr;
+    unsigned char* chg_in = memo ? scratch_flags : nullptr;
+    unsigned char* chg_out = memo ? scratch_flags + n_px : nullptr;
+    unsigned char* memo_valid = memo ? scratch_flags + 2 * n_px : nullptr;
+    double* memo_cost = memo ? scratch_memo : nullptr;
+    if (memo && (cudaMemsetAsync(chg_in, 1, n_px, s) != cudaSuccess ||
+                 cudaMemsetAsync(memo_valid, 0, n_px, s) != cudaSuccess)) {
+        set_error("cudaMemsetAsync(memo flags) failed");
         return 1;
     }
     for (int it = 0; it < iterations; ++it) {
         for (int parity = 0; parity < 2; ++parity) {
-            if (launch_red_black(gd, prec, parity, cd, cn, cc, nd, nn, nc, chg_in, chg_out, n_evals, s)) return 1;
+            if (launch_red_black(gd, prec, parity, cd, cn, cc, nd, nn, nc, chg_in, chg_out, memo_valid, memo_cost, n_evals, s))
+                return 1;
             float* tmp;
             tmp = cd; cd = nd; nd = tmp;
             tmp = cn; cn = nn; nn = tmp;

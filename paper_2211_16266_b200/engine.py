@@ -420,7 +420,10 @@ def random_init(plane_map: PlaneMap, depth_range, seed: int, rng: str = "pcg64")
 # ---------------------------------------------------------------------------------------
 
 def warp_plane_map_device(previous: DevicePlaneMap, pose_prev: RigidPose, pose_cur: RigidPose,
-                          camera: EquirectCamera) -> DevicePlaneMap:
+                          camera: EquirectCamera, winner: torch.Tensor | None = None) -> DevicePlaneMap:
+    """``winner``: optional (H, W) int64 scratch (the packed (cost, source) of the scatter); pass a
+    persistent one in a per-keyframe loop — a fresh 8 B/pixel allocation every call can miss the
+    caching allocator and cost a cudaMalloc (tens of ms) in the middle of a step."""
     if previous.camera != camera:
         raise ConfigError(f"plane map camera {previous.camera} does not match target camera {camera}")
     lib = _lib.load()
@@ -433,7 +436,8 @@ def warp_plane_map_device(previous: DevicePlaneMap, pose_prev: RigidPose, pose_c
     r_rel = np.ascontiguousarray(r_rel, np.float64)
     t_rel = np.ascontiguousarray(t_rel, np.float64)
     with torch.cuda.device(dev):
-        winner = torch.empty((h, w), dtype=torch.int64, device=dev)
+        if winner is None:
+            winner = torch.empty((h, w), dtype=torch.int64, device=dev)
         _lib.check(lib.d360_warp_plane_map(_ptr(previous.depth), _ptr(previous.normal), _ptr(previous.cost),
                                            _ptr(previous.valid), _ptr(cam.rays64), r_rel.ctypes.data,
                                            t_rel.ctypes.data, float(previous.depth_range[0]),
@@ -527,8 +531,10 @@ class PatchMatchWorkspace:
         self.depth = torch.empty((h, w), dtype=torch.float32, device=device)
         self.normal = torch.empty((h, w, 3), dtype=torch.float32, device=device)
         self.cost = torch.empty((h, w), dtype=torch.float32, device=device)
-        self.changed = torch.empty((2, h, w), dtype=torch.uint8, device=device)
+        self.flags = torch.empty((3, h, w), dtype=torch.uint8, device=device)    # changed (x2), memo validity
+        self.memo = torch.empty((h, w, 8), dtype=torch.float64, device=device)  # memoised candidate costs
         self.n_evals = torch.zeros((2,), dtype=torch.int64, device=device)  # [evaluations, cut short]
+        self.winner = torch.empty((h, w), dtype=torch.int64, device=device)  # scratch of warp_plane_map
 
 
 def run_patchmatch_device(prep: PreparedGroup, pm: DevicePlaneMap, iterations: int, seed: int,
@@ -541,9 +547,10 @@ def run_patchmatch_device(prep: PreparedGroup, pm: DevicePlaneMap, iterations: i
     One C-ABI call (d360_run_patchmatch) enqueues eval + iterations x (red, black, refine).
     With ``count_evals`` the executed propagation/refinement cost evaluations are ADDED to
     ``workspace.n_evals[0]`` and the refinement evaluations decided after V - 1 views to
-    ``workspace.n_evals[1]`` (zero it yourself; reading it synchronises).  ``skip_unchanged`` lets a
-    pixel skip re-testing neighbour hypotheses that did not change since the previous iteration
-    (result-neutral, see include/d360.h); switch it off to count the reference's evaluations."""
+    ``workspace.n_evals[1]`` (zero it yourself; reading it synchronises).  ``skip_unchanged`` lets
+    the propagation reuse the cost of a neighbour's hypothesis for as long as that hypothesis does
+    not change (memoised, bit-identical results, see include/d360.h); switch it off to count the
+    reference's evaluations."""
     if iterations < 1:
         raise ConfigError(f"patchmatch.iterations must be >= 1, got {iterations}")
     if prep.camera != pm.camera:
@@ -559,7 +566,8 @@ def run_patchmatch_device(prep: PreparedGroup, pm: DevicePlaneMap, iterations: i
         valid = torch.empty(prep.camera.shape, dtype=torch.uint8, device=prep.device)
         _lib.check(lib.d360_run_patchmatch(prep.struct, _ptr(pm.depth), _ptr(pm.normal), _ptr(pm.cost),
                                            _ptr(ws.depth), _ptr(ws.normal), _ptr(ws.cost),
-                                           _ptr(ws.changed) if skip_unchanged else 0, tables.ctypes.data,
+                                           _ptr(ws.flags) if skip_unchanged else 0,
+                                           _ptr(ws.memo) if skip_unchanged else 0, tables.ctypes.data,
                                            int(iterations), REFINE_CANDIDATES, float(dmin), float(dmax),
                                            _ptr(valid), _ptr(ws.n_evals) if count_evals else 0, _stream()),
                    "run_patchmatch")

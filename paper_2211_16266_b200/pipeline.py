@@ -173,7 +173,7 @@ class DepthStage:
         with torch.cuda.device(self.device):
             if self.warp and self._prev is not None:
                 prev_map, prev_pose = self._prev
-                init = warp_plane_map_device(prev_map, prev_pose, ref.pose, self.camera)
+                init = warp_plane_map_device(prev_map, prev_pose, ref.pose, self.camera, winner=self._ws.winner)
             else:
                 init = DevicePlaneMap.empty(self.camera, self.depth_range, self.device)
             init = random_init_device(init, self.depth_range, self.seed + ref.id, self.init_rng)
