@@ -185,7 +185,7 @@ def run_offline(keyframes, camera: EquirectCamera, *, viewfilter: ViewFilterConf
         t0 = time.perf_counter()
         jobs_before = stream.jobs
         for out in stream.push(keyframe):
-            filtered[out.id] = DepthResult(out.id, out.pano, out.pose, stream.image_of(out.id), 0.0)
+            filtered[out.id] = DepthResult(out.id, out.pano, out.pose, out.image, 0.0)
             if out.cloud is not None:
                 batches.append(out.cloud)
         dt = time.perf_counter() - t0

@@ -343,6 +343,7 @@ class StreamOutput:
     pano: DepthPanorama
     pose: RigidPose
     cloud: FusedCloud | None = None
+    image: np.ndarray | None = None  # the reference keyframe's host image (as given to push)
 
 
 class StreamingDensifier:
@@ -372,7 +373,7 @@ class StreamingDensifier:
         self._fusion = FusionBuffer(camera, fusion, self.device) if fusion is not None else None
         self._last_id = None
         self.jobs = 0       # depth jobs run so far
-        self._images = {}   # host image of every reference whose output is still pending
+        self._images = {}   # host image of every reference whose output is still pending (<= window entries)
 
     def push(self, keyframe: Keyframe) -> list:
         """Feed the next keyframe (ids strictly increasing); returns the outputs that
@@ -403,17 +404,13 @@ class StreamingDensifier:
         others = [(f.pano, f.pose) for i, f in enumerate(frames) if i != c]
         pano = consistency_filter_device(target.pano, target.pose, others, self.consistency)
         self._window.popleft()
-        out = StreamOutput(target.id, pano.to_host(), target.pose)
+        for old in [k for k in self._images if k < target.id]:
+            del self._images[old]  # references the consistency window left behind without an output
+        out = StreamOutput(target.id, pano.to_host(), target.pose, image=self._images.pop(target.id, None))
         if self._fusion is not None:
             batch = self._fusion.push_device(DeviceDepthResult(target.id, pano, target.pose, target.image))
             out.cloud = None if batch is None else batch.to_host()
         return [out]
-
-    def image_of(self, keyframe_id: int):
-        """Host image of a reference keyframe whose StreamOutput was just returned (handed over once)."""
-        for old in [k for k in self._images if k < keyframe_id]:
-            del self._images[old]  # frames the consistency window left behind without an output
-        return self._images.pop(keyframe_id)
 
     def finish(self) -> list:
         """Flush the fusion FIFO; frames still inside the consistency window are
