@@ -203,6 +203,7 @@ def run_product(args) -> dict | None:
     window = deque(maxlen=ccfg.window)
 
     dk_cache = {}  # keyframe index -> DeviceKeyframe (planes computed once, on first use)
+    group_buffers = {}  # the group's planes live in the same memory from step to step
 
     def device_keyframe(idx):
         dk = dk_cache.get(idx)
@@ -215,7 +216,7 @@ def run_product(args) -> dict | None:
     def step_device(i):
         flush_buf.zero_()  # L2 flush (256 MiB > 126 MB L2), inside the timed region
         g = group_of(i)
-        prep = engine.PreparedGroup(g, spec, precision=args.precision, device=dev,
+        prep = engine.PreparedGroup(g, spec, precision=args.precision, device=dev, buffers=group_buffers,
                                     device_keyframes=[device_keyframe(i)] + [device_keyframe(i + o) for o in nb_order])
         res = stage.process_device(prep)
         window.append(res)

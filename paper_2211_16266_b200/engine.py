@@ -291,10 +291,14 @@ class PreparedGroup:
 
     ``device_images``: optional uint8 CUDA tensors (reference first) instead of the keyframes'
     host images; ``device_keyframes``: optional ``DeviceKeyframe`` list (reference first) whose
-    cached planes are gathered instead of recomputing the luma."""
+    cached planes are gathered instead of recomputing the luma; ``buffers``: optional dict a
+    per-keyframe loop passes again and again — the group's planes (180 MB at 1920x960, V = 4) then
+    live in the same memory for every group of the stream instead of going through the allocator
+    (the previous group must no longer be in use; work on one stream is ordered anyway)."""
 
     def __init__(self, group: StereoGroup, spec: PatchSpec, top_k: int | None = None,
-                 precision: str | None = None, device=None, device_images=None, device_keyframes=None):
+                 precision: str | None = None, device=None, device_images=None, device_keyframes=None,
+                 buffers: dict | None = None):
         self.group = group
         self.spec = spec
         self.camera = group.camera
@@ -314,9 +318,16 @@ class PreparedGroup:
             h, w = self.camera.shape
             # neighbour luma planes, padded so that every bilinear footprint is in-plane (d360.h),
             # and the same planes widened to f64: the reference interpolates in f64 (K:134-153)
-            self.nb_padded = torch.empty((self.n_views, h + 2 * NB_PAD_Y, w + 2 * NB_PAD_X), dtype=torch.float32,
-                                         device=self.device)
-            self.nb64_padded = torch.empty((*self.nb_padded.shape, 2), dtype=torch.float64, device=self.device)
+            def plane(name, shape, dtype):
+                if buffers is None:
+                    return torch.empty(shape, dtype=dtype, device=self.device)
+                t = buffers.get(name)
+                if t is None or tuple(t.shape) != tuple(shape) or t.dtype != dtype or t.device != self.device:
+                    t = buffers[name] = torch.empty(shape, dtype=dtype, device=self.device)
+                return t
+
+            self.nb_padded = plane("nb32", (self.n_views, h + 2 * NB_PAD_Y, w + 2 * NB_PAD_X), torch.float32)
+            self.nb64_padded = plane("nb64", (*self.nb_padded.shape, 2), torch.float64)
             if device_keyframes is not None:
                 if len(device_keyframes) != self.n_views + 1:
                     raise ValueError("device_keyframes must list the reference and every neighbour")
@@ -338,8 +349,7 @@ class PreparedGroup:
             # (ray, luma) of the reference as one padded float4 plane: the TMA source of the patch windows
             self.ref_ctx = None
             if self.precision == "mixed":
-                self.ref_ctx = torch.empty((h + 2 * REF_CTX_PAD, w + 2 * REF_CTX_PAD, 4), dtype=torch.float32,
-                                           device=self.device)
+                self.ref_ctx = plane("ctx", (h + 2 * REF_CTX_PAD, w + 2 * REF_CTX_PAD, 4), torch.float32)
                 _lib.check(_lib.load().d360_build_ref_context(_ptr(self.cam_dev.rays32), _ptr(self.ref_gray),
                                                               _ptr(self.ref_ctx), h, w, REF_CTX_PAD, _stream()),
                            "build_ref_context")

@@ -372,6 +372,7 @@ class StreamingDensifier:
         self._window: deque = deque()                        # DeviceDepthResult
         self._fusion = FusionBuffer(camera, fusion, self.device) if fusion is not None else None
         self._last_id = None
+        self._group_buffers = {}  # planes of the group in flight, reused from push to push
         self.jobs = 0       # depth jobs run so far
         self._images = {}   # host image of every reference whose output is still pending (<= window entries)
 
@@ -392,7 +393,8 @@ class StreamingDensifier:
         group = StereoGroup(reference=self._frames[mid][0], neighbors=tuple(self._frames[i][0] for i in picks[1:]),
                             camera=self.camera)
         prep = PreparedGroup(group, self.stage.spec, top_k=self.stage.top_k, precision=self.stage.precision,
-                             device=self.device, device_keyframes=[self._frames[i][1] for i in picks])
+                             device=self.device, device_keyframes=[self._frames[i][1] for i in picks],
+                             buffers=self._group_buffers)
         self._window.append(self.stage.process_device(prep))
         self.jobs += 1
         self._images[group.reference.id] = group.reference.image
