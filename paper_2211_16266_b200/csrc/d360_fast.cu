@@ -84,7 +84,9 @@ bool make_fast_group(const GroupDev& gd, FastGroup* out) {
                                  -1.404782123164e-01, 1.997402857787e-01, -3.333223261885e-01, 9.999999227776e-01};
     static const double CQ[8] = {-1.223553911532e-03, 6.510368059701e-03, -1.682974898800e-02, 3.068214201158e-02,
                                  -5.008467775423e-02, 8.895977933699e-02, -2.145970563340e-01, 1.570796263346e00};
-    for (int i = 0; i < 8; ++i) { g.ca[i] = CA[i]; g.cq[i] = CQ[i]; }
+    for (int i = 0; i < 8; ++i) { g.ca[i] = CA[i] / CA[0]; g.cq[i] = CQ[i] / CQ[0]; }  // monic, see project_uv
+    for (int oct = 0; oct < 8; ++oct) g.mu[oct] *= CA[0];
+    for (int hem = 0; hem < 2; ++hem) g.mv[hem] *= CQ[0];
     if ((unsigned long long)(pitch * rows) * (unsigned long long)gd.V >= (1ull << 32)) return false;
     g.plane32 = (unsigned)(pitch * rows);
     g.neg_par_eps = -D360_PARALLEL_EPS;

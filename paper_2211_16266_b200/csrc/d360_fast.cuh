@@ -51,7 +51,8 @@ struct FastGroup {
     double rel_t[D360_MAX_VIEWS][3];
     double mu[8], cu[8];  // longitude: u = p * mu[oct] + cu[oct]
     double mv[2], cv[2];  // latitude:  v = p * mv[hem] + cv[hem]
-    double ca[8], cq[8];  // atan / acos polynomial coefficients, highest degree first (K:75-85, K:112-122)
+    double ca[8], cq[8];  // atan / acos polynomial coefficients (K:75-85, K:112-122), highest degree first,
+                          // divided by the leading one ([0] unused; it is folded into mu / mv)
     double trunc, inv_s;
     double neg_par_eps, tiny, c0375;  // -PARALLEL_EPS, 1e-30 (K:246), 3/8: 64-bit literals live in the constant bank
     unsigned plane32;     // plane as a 32-bit element count
@@ -276,10 +277,13 @@ __device__ __forceinline__ void project_uv(const FastGroup& g, const double (&tx
     D360_FORV { r[v] = lo[v] * y3[v]; s[v] = r[v] * r[v]; }
 #pragma unroll
     D360_FORV { w[v] = 1.0 - a[v]; y2[v] = rsqrt_seed(w[v]); }
+    // Horner on the monic polynomials (coefficients divided by the leading one, which is folded
+    // into the mu / mv tables): the first step is an add with one constant operand instead of an
+    // FMA with two, which would cost two register moves per polynomial.
 #pragma unroll
-    D360_FORV { q[v] = g.cq[0]; p[v] = g.ca[0]; }
+    D360_FORV { q[v] = a[v] + g.cq[1]; p[v] = s[v] + g.ca[1]; }
 #pragma unroll
-    for (int i = 1; i < 8; ++i) {
+    for (int i = 2; i < 8; ++i) {
 #pragma unroll
         D360_FORV { q[v] = fma(a[v], q[v], g.cq[i]); p[v] = fma(s[v], p[v], g.ca[i]); }
     }
