@@ -328,10 +328,11 @@ __device__ __forceinline__ void gather_bilinear(const FastGroup& g, const double
     double2 r0[VT], r1[VT];  // { value, value(x+1) - value }
 #pragma unroll
     D360_FORV {
-        const double2* __restrict__ row0 = nb + (size_t)(v % PERIOD) * plane_stride;  // uniform per view
-        const double2* __restrict__ row1 = row0 + g.pitch;
-        r0[v] = __ldg(row0 + idx[v]);
-        r1[v] = __ldg(row1 + idx[v]);
+        // 32-bit element indices from one base (all planes together hold < 2^32 texels): one integer
+        // add and one IMAD.WIDE per load; 64-bit per-view bases cost four instructions per load
+        const unsigned i0 = idx[v] + (unsigned)(v % PERIOD) * plane_stride;
+        r0[v] = __ldg(nb + i0);
+        r1[v] = __ldg(nb + (i0 + (unsigned)g.pitch));
     }
 #pragma unroll
     D360_FORV {
