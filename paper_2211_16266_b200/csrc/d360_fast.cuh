@@ -315,14 +315,21 @@ template <int VT, int PERIOD = VT>
 __device__ __forceinline__ void gather_bilinear(const FastGroup& g, const double2* __restrict__ nb,
                                                 unsigned plane_stride, const float (&pu)[VT], const float (&pv)[VT],
                                                 double (&val)[VT]) {
-    const float MAGIC = 12582912.0f;  // 1.5 * 2^23: (x + MAGIC) rounded towards -inf is floor(x) + MAGIC
-    float fl_u[VT], fl_v[VT];
+    // floor by a round-down add of a magic constant: (x + M) rounded towards -inf is floor(x) + M for
+    // an integer M in [2^23, 2^24) (ulp 1).  For u the constant is idx_bias = 2^23 + pad_y * pitch +
+    // pad_x, so the biased floor is already the low part of the texel index.
+    const float MAGIC = 12582912.0f;  // 1.5 * 2^23
+    float fl_u[VT], fl_v[VT], bu[VT];
 #pragma unroll
-    D360_FORV { fl_u[v] = __fadd_rn(__fadd_rd(pu[v], MAGIC), -MAGIC); fl_v[v] = __fadd_rn(__fadd_rd(pv[v], MAGIC), -MAGIC); }
+    D360_FORV {
+        bu[v] = __fadd_rd(pu[v], g.idx_bias);
+        fl_u[v] = __fadd_rn(bu[v], -g.idx_bias);
+        fl_v[v] = __fadd_rn(__fadd_rd(pv[v], MAGIC), -MAGIC);
+    }
     unsigned idx[VT];
 #pragma unroll
     D360_FORV {
-        const float off = __fadd_rn(fmaf(fl_v[v], g.pitch_f, fl_u[v]), g.idx_bias);
+        const float off = fmaf(fl_v[v], g.pitch_f, bu[v]);  // exact: < 2^24
         idx[v] = min((unsigned)__float_as_int(off) & 0x7fffffu, g.max_idx);
     }
     double2 r0[VT], r1[VT];  // { value, value(x+1) - value }
