@@ -379,10 +379,17 @@ __device__ __forceinline__ double aggregate(double (&cv)[NV], int top_k) {
 template <class C, typename HT, int V0, int NV, int SPT>
 __device__ __forceinline__ void accumulate_views_multi(const FastGroup& g, const Tile& t, int ce, double num, HT nx,
                                                        HT ny, HT nz, bool& bad, double (&s0)[NV], double (&ss0)[NV],
-                                                       double (&rs0)[NV]) {
+                                                       double (&rs0)[NV], int vbase = 0) {
+    // vbase: run-time view offset added to V0 (only the sparse-tile path of red_black_pass, where
+    // the lanes of a warp work on different views, passes anything but 0)
 #pragma unroll
     for (int v = 0; v < NV; ++v) s0[v] = ss0[v] = rs0[v] = 0.0;
-    const double2* __restrict__ nb = reinterpret_cast<const double2*>(g.nb64) + (size_t)V0 * g.plane32;
+    const double2* __restrict__ nb = reinterpret_cast<const double2*>(g.nb64) + (size_t)(V0 + vbase) * g.plane32;
+    double rel[NV][3];
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) rel[v][c] = g.rel_t[V0 + vbase + v][c];
     auto plane_depth = [&](int es, double& lam, double& rv) {
         const float4 q = t.qg[es];
         double dn;
@@ -403,7 +410,7 @@ __device__ __forceinline__ void accumulate_views_multi(const FastGroup& g, const
     const int half = (ns - 1) / 2;
     const int n_samples = ns * ns;
     const int row_wrap = t.sy - ns * t.sx;
-    const double* rq0 = t.rq + V0 * 3 * t.ne;
+    const double* rq0 = t.rq + (V0 + vbase) * 3 * t.ne;
     int e = ce - half * (t.sx + t.sy), col = 0;
     auto next_entry = [&](int cur) {
         int nxt = cur + t.sx;
@@ -426,9 +433,9 @@ __device__ __forceinline__ void accumulate_views_multi(const FastGroup& g, const
         for (int j = 0; j < SPT; ++j) {
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
-                tx[j * NV + v] = fma(lam[j], rq0[(v * 3 + 0) * t.ne + es[j]], g.rel_t[V0 + v][0]);
-                ty[j * NV + v] = fma(lam[j], rq0[(v * 3 + 1) * t.ne + es[j]], g.rel_t[V0 + v][1]);
-                tz[j * NV + v] = fma(lam[j], rq0[(v * 3 + 2) * t.ne + es[j]], g.rel_t[V0 + v][2]);
+                tx[j * NV + v] = fma(lam[j], rq0[(v * 3 + 0) * t.ne + es[j]], rel[v][0]);
+                ty[j * NV + v] = fma(lam[j], rq0[(v * 3 + 1) * t.ne + es[j]], rel[v][1]);
+                tz[j * NV + v] = fma(lam[j], rq0[(v * 3 + 2) * t.ne + es[j]], rel[v][2]);
             }
         }
         project_uv<SPT * NV>(g, tx, ty, tz, pu, pv);
@@ -450,9 +457,9 @@ __device__ __forceinline__ void accumulate_views_multi(const FastGroup& g, const
         plane_depth(e, lam, rv);
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
-            tx[v] = fma(lam, rq0[(v * 3 + 0) * t.ne + e], g.rel_t[V0 + v][0]);
-            ty[v] = fma(lam, rq0[(v * 3 + 1) * t.ne + e], g.rel_t[V0 + v][1]);
-            tz[v] = fma(lam, rq0[(v * 3 + 2) * t.ne + e], g.rel_t[V0 + v][2]);
+            tx[v] = fma(lam, rq0[(v * 3 + 0) * t.ne + e], rel[v][0]);
+            ty[v] = fma(lam, rq0[(v * 3 + 1) * t.ne + e], rel[v][1]);
+            tz[v] = fma(lam, rq0[(v * 3 + 2) * t.ne + e], rel[v][2]);
         }
         project_uv<NV>(g, tx, ty, tz, pu, pv);
         gather_bilinear<NV>(g, nb, g.plane32, pu, pv, val);
@@ -580,6 +587,32 @@ __device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, i
     }
     const double total = aggregate<VT>(cv, g.top_k);
     return total == total ? total : trunc;  // NaN only from the unguarded polar singularities
+}
+
+// NVL consecutive views (from the run-time view `view0`) of the same evaluation (f32 hypothesis):
+// the per-view costs cand_cost would compute for them, bit for bit (a view's sums see the samples
+// in the same order whether its chains run next to other views' chains or alone).  `whole` is
+// cleared when the evaluation as a whole scores `trunc` (facing / sigma guard, poisoned sample):
+// that decision does not depend on the views.
+template <class C, int NVL>
+__device__ __forceinline__ void cand_views_cost(const FastGroup& g, const Tile& t, int ce, int view0, double mr,
+                                                double sr, float d, float nx, float ny, float nz, bool& whole,
+                                                double (&cv)[NVL]) {
+#pragma unroll
+    for (int v = 0; v < NVL; ++v) cv[v] = g.trunc;
+    const float4 a = t.qg[ce];
+    const float ndota = dot3_f32(nx, ny, nz, a.x, a.y, a.z);
+    if ((double)ndota >= -D360_FACING_EPS || sr < D360_SIGMA_EPS) {
+        whole = false;
+        return;
+    }
+    const double num = (double)__fmul_rn(d, ndota);
+    bool bad = false;
+    double s0[NVL], ss0[NVL], rs0[NVL];
+    accumulate_views_multi<C, float, 0, NVL, D360_SPT>(g, t, ce, num, nx, ny, nz, bad, s0, ss0, rs0, view0);
+    if (bad) whole = false;
+#pragma unroll
+    for (int v = 0; v < NVL; ++v) cv[v] = view_cost<true>(g, s0[v], ss0[v], rs0[v], mr, sr);
 }
 
 // host side, d360_fast.cu

@@ -222,24 +222,74 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
             q.stats[tid] = make_double2(mr, sr);
         }
         __syncthreads();
-        for (;;) {
-            int base = 0;
-            if ((tid & 31) == 0) base = atomicAdd(&q.next, 32);
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (base >= total) break;
-            const int it = base + (tid & 31);
-            if (it < total) {
-                const int item = q.items[it];
-                const int p = item >> 3, j = item & 7;
-                const int ply = p / (TW / 2);
-                const int py = y0 + ply;
-                const int plx = 2 * (p % (TW / 2)) + ((parity + py) & 1);
-                const int px = x0 + plx;
-                const size_t qi = (size_t)(py + c_nbr2[j][1]) * g.W + wrap_once(px + c_nbr2[j][0], g.W);
-                const int ce = (ply + R) * t.wwc + (compress ? (plx + R) >> 1 : plx + R);
-                const double2 st = q.stats[p];
-                q.costs[item] = cand_cost<C, float>(g, t, ce, st.x, st.y, depth_in[qi], normal_in[3 * qi],
-                                                    normal_in[3 * qi + 1], normal_in[3 * qi + 2]);
+        // Sparse tile (late iterations: a handful of candidates per CTA): the pass is then bound by
+        // the latency of one evaluation per CTA, so an item is spread over 4 lanes (one view each)
+        // or 2 lanes (two views each) as far as the CTA's lanes go round.  The per-view costs are
+        // the ones the joint evaluation computes, bit for bit, so memoised and fresh costs stay
+        // interchangeable.
+        int lanes_per_item = 1;
+        if constexpr (C::V == 4) lanes_per_item = total <= NT / 4 ? 4 : (total <= NT / 2 ? 2 : 1);
+        if (lanes_per_item > 1) {
+            if constexpr (C::V == 4) {
+                const int slot = lanes_per_item == 4 ? tid >> 2 : tid >> 1;
+                const int part = lanes_per_item == 4 ? tid & 3 : tid & 1;
+                if (slot < total) {  // uniform within the lane group
+                    const int item = q.items[slot];
+                    const int p = item >> 3, j = item & 7;
+                    const int ply = p / (TW / 2);
+                    const int py = y0 + ply;
+                    const int plx = 2 * (p % (TW / 2)) + ((parity + py) & 1);
+                    const int px = x0 + plx;
+                    const size_t qi = (size_t)(py + c_nbr2[j][1]) * g.W + wrap_once(px + c_nbr2[j][0], g.W);
+                    const int ce = (ply + R) * t.wwc + (compress ? (plx + R) >> 1 : plx + R);
+                    const double2 st = q.stats[p];
+                    const float hd0 = depth_in[qi], hx0 = normal_in[3 * qi], hy0 = normal_in[3 * qi + 1],
+                                hz0 = normal_in[3 * qi + 2];
+                    bool whole = true;
+                    double cv[4];
+                    if (lanes_per_item == 4) {
+                        double mine[1];
+                        cand_views_cost<C, 1>(g, t, ce, part, st.x, st.y, hd0, hx0, hy0, hz0, whole, mine);
+                        const unsigned group = 0xfu << (tid & 28);
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) cv[v] = __shfl_sync(group, mine[0], (tid & 28) + v);
+                    } else {
+                        double mine[2];
+                        cand_views_cost<C, 2>(g, t, ce, 2 * part, st.x, st.y, hd0, hx0, hy0, hz0, whole, mine);
+                        const unsigned group = 0x3u << (tid & 30);
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) cv[v] = __shfl_sync(group, mine[v & 1], (tid & 30) + (v >> 1));
+                    }
+                    if (part == 0) {
+                        double c = g.trunc;
+                        if (whole) {
+                            const double agg = aggregate<4>(cv, g.top_k);
+                            c = agg == agg ? agg : g.trunc;
+                        }
+                        q.costs[item] = c;
+                    }
+                }
+            }
+        } else {
+            for (;;) {
+                int base = 0;
+                if ((tid & 31) == 0) base = atomicAdd(&q.next, 32);
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (base >= total) break;
+                const int it = base + (tid & 31);
+                if (it < total) {
+                    const int item = q.items[it];
+                    const int p = item >> 3, j = item & 7;
+                    const int ply = p / (TW / 2);
+                    const int py = y0 + ply;
+                    const int plx = 2 * (p % (TW / 2)) + ((parity + py) & 1);
+                    const int px = x0 + plx;
+                    const size_t qi = (size_t)(py + c_nbr2[j][1]) * g.W + wrap_once(px + c_nbr2[j][0], g.W);
+                    const int ce = (ply + R) * t.wwc + (compress ? (plx + R) >> 1 : plx + R);
+                    const double2 st = q.stats[p];
+                    q.costs[item] = cand_cost<C, float>(g, t, ce, st.x, st.y, depth_in[qi], normal_in[3 * qi],
+                                                        normal_in[3 * qi + 1], normal_in[3 * qi + 2]);
+                }
             }
         }
         __syncthreads();
