@@ -69,24 +69,36 @@ bool make_fast_group(const GroupDev& gd, FastGroup* out) {
         for (int i = 0; i < 3; ++i) g.rel_t[v][i] = (double)gd.rel_t[v][i];
     }
     const double hw = gd.W * (0.5 / D360_PI), ls = gd.H / D360_PI;
-    for (int oct = 0; oct < 8; ++oct) {
-        const bool swap = oct & 1, xneg = oct & 2, yneg = oct & 4;
-        // theta = sy * (cx + sx * (cs + ss * p)), K:96-99
-        const double ss = swap ? -1.0 : 1.0, cs = swap ? D360_HALF_PI : 0.0;
-        const double sx = xneg ? -1.0 : 1.0, cx = xneg ? D360_PI : 0.0;
-        const double sy = yneg ? -1.0 : 1.0;
-        g.mu[oct] = sy * sx * ss * hw;
-        g.cu[oct] = (sy * (cx + sx * cs) + D360_PI) * hw - 0.5;
-    }
-    g.mv[1] = ls;  g.cv[1] = -0.5;                  // ty < 0: sphi > 0
-    g.mv[0] = -ls; g.cv[0] = D360_PI * ls - 0.5;    // ty > 0: sphi < 0, acos = pi - p (K:131)
     static const double CA[8] = {-5.021063913876e-03, 2.533170107199e-02, -6.087448223083e-02, 1.000220525649e-01,
                                  -1.404782123164e-01, 1.997402857787e-01, -3.333223261885e-01, 9.999999227776e-01};
     static const double CQ[8] = {-1.223553911532e-03, 6.510368059701e-03, -1.682974898800e-02, 3.068214201158e-02,
                                  -5.008467775423e-02, 8.895977933699e-02, -2.145970563340e-01, 1.570796263346e00};
-    for (int i = 0; i < 8; ++i) { g.ca[i] = CA[i] / CA[0]; g.cq[i] = CQ[i] / CQ[0]; }  // monic, see project_uv
-    for (int oct = 0; oct < 8; ++oct) g.mu[oct] *= CA[0];
-    for (int hem = 0; hem < 2; ++hem) g.mv[hem] *= CQ[0];
+    // acos polynomial (K:112-122) re-expanded in w = 1 - x: q(1 - w) by repeated synthetic division at
+    // x = 1 (Taylor shift) in extended precision, then the sign of the odd powers of (x - 1) = -w
+    long double cw[8];  // ascending powers
+    for (int i = 0; i < 8; ++i) cw[i] = (long double)CQ[7 - i];
+    for (int i = 0; i < 7; ++i)
+        for (int j = 6; j >= i; --j) cw[j] += cw[j + 1];
+    for (int i = 1; i < 8; i += 2) cw[i] = -cw[i];
+#if !D360_W_FUSED
+    for (int i = 0; i < 8; ++i) cw[i] = (long double)CQ[7 - i];
+#endif
+    for (int i = 0; i < 8; ++i) {  // monic, highest degree first, see project_uv
+        g.ca[i] = CA[i] / CA[0];
+        g.cq[i] = (double)(cw[7 - i] / cw[7]);
+    }
+    for (int k = 0; k < fast::OCT_SLOTS; ++k) g.uo[k] = make_double2(0.0, 0.0);
+    for (int oct = 0; oct < 8; ++oct) {
+        const bool swap = oct & 1, xneg = oct & 2, yneg = oct & 4;
+        // theta = sy * (cx + sx * (cs + ss * p)), K:96-99 with y = tx, x = tz
+        const double ss = swap ? -1.0 : 1.0, cs = swap ? D360_HALF_PI : 0.0;
+        const double sx = xneg ? -1.0 : 1.0, cx = xneg ? D360_PI : 0.0;
+        const double sy = yneg ? -1.0 : 1.0;
+        const int slot = (yneg ? fast::OCT_SX : 0) + (xneg ? fast::OCT_SZ : 0) + (swap ? fast::OCT_SW : 0);
+        g.uo[slot] = make_double2(sy * sx * ss * hw * CA[0], (sy * (cx + sx * cs) + D360_PI) * hw - 0.5);
+    }
+    g.vo[1] = make_double2(ls * (double)cw[7], -0.5);                   // ty < 0: sphi > 0
+    g.vo[0] = make_double2(-ls * (double)cw[7], D360_PI * ls - 0.5);    // ty > 0: sphi < 0, acos = pi - p (K:131)
     if ((unsigned long long)(pitch * rows) * (unsigned long long)gd.V >= (1ull << 32)) return false;
     g.plane32 = (unsigned)(pitch * rows);
     g.neg_par_eps = -D360_PARALLEL_EPS;

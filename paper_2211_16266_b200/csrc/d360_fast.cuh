@@ -31,7 +31,12 @@ namespace d360 {
 namespace fast {
 
 constexpr int TW = 32;  // tile width (pixels)
+// octant table slots, in 16-byte entries (FastGroup::uo)
+constexpr int OCT_SX = 1, OCT_SZ = 16, OCT_SW = 4, OCT_SLOTS = OCT_SX + OCT_SZ + OCT_SW + 1;
 
+#ifndef D360_W_FUSED
+#define D360_W_FUSED 1
+#endif
 #ifndef D360_NT
 #define D360_NT 256  // threads per CTA
 #endif
@@ -49,10 +54,13 @@ struct FastGroup {
     const double* nb64;   // padded planes widened to f64, two doubles per texel, see d360.h
     float rel_r[D360_MAX_VIEWS][9];
     double rel_t[D360_MAX_VIEWS][3];
-    double mu[8], cu[8];  // longitude: u = p * mu[oct] + cu[oct]
-    double mv[2], cv[2];  // latitude:  v = p * mv[hem] + cv[hem]
-    double ca[8], cq[8];  // atan / acos polynomial coefficients (K:75-85, K:112-122), highest degree first,
-                          // divided by the leading one ([0] unused; it is folded into mu / mv)
+    // longitude: u = p * uo[k].x + uo[k].y, k = OCT_SX * (tx < 0) + OCT_SZ * (tz < 0) + OCT_SW * (|tx| > |tz|):
+    // the slots a byte permute of the two sign bytes plus one predicated OR can address (see project_uv)
+    double2 uo[OCT_SLOTS];
+    double2 vo[2];        // latitude: v = p * vo[ty >= 0].x + vo[ty >= 0].y  (index 1: ty < 0)
+    double ca[8], cq[8];  // atan polynomial in s = (lo / hi)^2 (K:75-85) and acos polynomial re-expanded in
+                          // w = 1 - |sphi| (K:112-122), highest degree first, divided by the leading
+                          // coefficient ([0] unused; it is folded into uo / vo)
     double trunc, inv_s;
     double neg_par_eps, tiny, c0375;  // -PARALLEL_EPS, 1e-30 (K:246), 3/8: 64-bit literals live in the constant bank
     unsigned plane32;     // plane as a 32-bit element count
@@ -82,7 +90,10 @@ struct Cfg {
 // neighbouring lanes read neighbouring slots.
 struct Tile {
     const float4* qg;  // (qx, qy, qz, reference luma) per entry
-    const double* rq;  // [(v*3 + c) * ne + entry]  R_v q as f64 (exact widening of the f32 dot, K:184-189)
+    // R_v q as f64 (exact widening of the f32 dot, K:184-189), laid out for 16-byte loads:
+    // rxy[v * ne + entry] = (x, y) of view v;  rz[(v / 2) * ne + entry] = z of views (v & ~1, v | 1)
+    const double2* rxy;
+    const double2* rz;
     int wwc;           // entries per window row
     int ne;            // entries per plane
     int sx, sy;        // entry step of one sample column / row
@@ -94,7 +105,25 @@ __host__ __device__ inline int window_entries(int tw, int th, int reach, bool co
 }
 __host__ __device__ inline size_t tile_bytes(int tw, int th, int reach, bool compress, int n_views) {
     const size_t ne = (size_t)window_entries(tw, th, reach, compress);
-    return ne * sizeof(float4) + ne * sizeof(double) * 3 * n_views;
+    return ne * sizeof(float4) + ne * sizeof(double2) * (n_views + (n_views + 1) / 2);
+}
+
+// R_v q of window entry e for all views, from its ray q
+template <class C>
+__device__ __forceinline__ void store_rq(const FastGroup& g, double2* rxy, double2* rz, int ne, int e, float qx,
+                                         float qy, float qz) {
+#pragma unroll
+    for (int v = 0; v < C::V; v += 2) {
+        double z[2] = {0.0, 0.0};
+#pragma unroll
+        for (int h = 0; h < 2 && v + h < C::V; ++h) {
+            const float* r = g.rel_r[v + h];
+            rxy[(v + h) * ne + e] = make_double2((double)dot3_f32(r[0], r[1], r[2], qx, qy, qz),
+                                                 (double)dot3_f32(r[3], r[4], r[5], qx, qy, qz));
+            z[h] = (double)dot3_f32(r[6], r[7], r[8], qx, qy, qz);
+        }
+        rz[(v >> 1) * ne + e] = make_double2(z[0], z[1]);
+    }
 }
 
 __host__ __device__ inline size_t mbar_offset(size_t tile) { return (tile + 15) & ~(size_t)15; }
@@ -107,7 +136,8 @@ __device__ __forceinline__ Tile tile_setup(const FastGroup& g, unsigned char* sm
     const int wwc = compress ? ww / 2 : ww;
     const int ne = wwc * hh;
     float4* qg = reinterpret_cast<float4*>(smem);
-    double* rq = reinterpret_cast<double*>(smem + (size_t)ne * sizeof(float4));
+    double2* rxy = reinterpret_cast<double2*>(smem + (size_t)ne * sizeof(float4));
+    double2* rz = rxy + (size_t)C::V * ne;
     for (int e = threadIdx.x; e < ne; e += C::NT) {
         const int j = e / wwc, ic = e - j * wwc;
         const int i = compress ? 2 * ic + ((keep + j) & 1) : ic;
@@ -116,17 +146,12 @@ __device__ __forceinline__ Tile tile_setup(const FastGroup& g, unsigned char* sm
         const size_t gi = (size_t)gy * g.W + gx;
         const float bx = __ldg(g.rays + 3 * gi), by = __ldg(g.rays + 3 * gi + 1), bz = __ldg(g.rays + 3 * gi + 2);
         qg[e] = make_float4(bx, by, bz, __ldg(g.ref_gray + gi));
-#pragma unroll
-        for (int v = 0; v < C::V; ++v) {
-            const float* r = g.rel_r[v];
-            rq[(v * 3 + 0) * ne + e] = (double)dot3_f32(r[0], r[1], r[2], bx, by, bz);
-            rq[(v * 3 + 1) * ne + e] = (double)dot3_f32(r[3], r[4], r[5], bx, by, bz);
-            rq[(v * 3 + 2) * ne + e] = (double)dot3_f32(r[6], r[7], r[8], bx, by, bz);
-        }
+        store_rq<C>(g, rxy, rz, ne, e, bx, by, bz);
     }
     Tile t;
     t.qg = qg;
-    t.rq = rq;
+    t.rxy = rxy;
+    t.rz = rz;
     t.wwc = wwc;
     t.ne = ne;
     t.sx = compress ? C::stride(g) / 2 : C::stride(g);
@@ -155,7 +180,8 @@ __device__ __forceinline__ Tile tile_setup_tma(const FastGroup& g, const WindowM
     const int ww = TW + 2 * R, hh = th + 2 * R;
     const int ne = ww * hh;
     float4* qg = reinterpret_cast<float4*>(smem);
-    double* rq = reinterpret_cast<double*>(smem + (size_t)ne * sizeof(float4));
+    double2* rxy = reinterpret_cast<double2*>(smem + (size_t)ne * sizeof(float4));
+    double2* rz = rxy + (size_t)C::V * ne;
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -183,17 +209,12 @@ __device__ __forceinline__ Tile tile_setup_tma(const FastGroup& g, const WindowM
     }
     for (int e = threadIdx.x; e < ne; e += C::NT) {
         const float4 q = qg[e];
-#pragma unroll
-        for (int v = 0; v < C::V; ++v) {
-            const float* r = g.rel_r[v];
-            rq[(v * 3 + 0) * ne + e] = (double)dot3_f32(r[0], r[1], r[2], q.x, q.y, q.z);
-            rq[(v * 3 + 1) * ne + e] = (double)dot3_f32(r[3], r[4], r[5], q.x, q.y, q.z);
-            rq[(v * 3 + 2) * ne + e] = (double)dot3_f32(r[6], r[7], r[8], q.x, q.y, q.z);
-        }
+        store_rq<C>(g, rxy, rz, ne, e, q.x, q.y, q.z);
     }
     Tile t;
     t.qg = qg;
-    t.rq = rq;
+    t.rxy = rxy;
+    t.rz = rz;
     t.wwc = ww;
     t.ne = ne;
     t.sx = C::stride(g);
@@ -246,7 +267,7 @@ __device__ __forceinline__ double rcp3(double x) {
 template <int VT>
 __device__ __forceinline__ void project_uv(const FastGroup& g, const double (&tx)[VT], const double (&ty)[VT],
                                            const double (&tz)[VT], float (&pu)[VT], float (&pv)[VT]) {
-    double r2[VT], y1[VT], e1[VT], a[VT], q[VT], w[VT], y2[VT], e2[VT], sq[VT];
+    double r2[VT], y1[VT], e1[VT], q[VT], w[VT], y2[VT], e2[VT], sq[VT];
 #pragma unroll
     D360_FORV r2[v] = fma(tz[v], tz[v], fma(ty[v], ty[v], fma(tx[v], tx[v], g.tiny)));
 #pragma unroll
@@ -270,23 +291,31 @@ __device__ __forceinline__ void project_uv(const FastGroup& g, const double (&tx
     D360_FORV y1[v] = fma(y1[v] * e1[v], fma(e1[v], g.c0375, 0.5), y1[v]);
 #pragma unroll
     D360_FORV y3[v] = fma(y3[v], fma(e3[v], e3[v], e3[v]), y3[v]);
-#pragma unroll
-    D360_FORV a[v] = fabs(ty[v]) * y1[v];
     double r[VT], s[VT], p[VT];
 #pragma unroll
     D360_FORV { r[v] = lo[v] * y3[v]; s[v] = r[v] * r[v]; }
+    // w = 1 - |sphi| = 1 - |ty| / |t| in one rounding; the acos polynomial is expanded in w
 #pragma unroll
-    D360_FORV { w[v] = 1.0 - a[v]; y2[v] = rsqrt_seed(w[v]); }
+#if D360_W_FUSED
+    D360_FORV { w[v] = fma(-fabs(ty[v]), y1[v], 1.0); y2[v] = rsqrt_seed(w[v]); }
+#else
+    double a[VT];
+    D360_FORV { a[v] = fabs(ty[v]) * y1[v]; w[v] = 1.0 - a[v]; y2[v] = rsqrt_seed(w[v]); }
+#define w a
+#endif
     // Horner on the monic polynomials (coefficients divided by the leading one, which is folded
-    // into the mu / mv tables): the first step is an add with one constant operand instead of an
+    // into the uo / vo tables): the first step is an add with one constant operand instead of an
     // FMA with two, which would cost two register moves per polynomial.
 #pragma unroll
-    D360_FORV { q[v] = a[v] + g.cq[1]; p[v] = s[v] + g.ca[1]; }
+    D360_FORV { q[v] = w[v] + g.cq[1]; p[v] = s[v] + g.ca[1]; }
 #pragma unroll
     for (int i = 2; i < 8; ++i) {
 #pragma unroll
-        D360_FORV { q[v] = fma(a[v], q[v], g.cq[i]); p[v] = fma(s[v], p[v], g.ca[i]); }
+        D360_FORV { q[v] = fma(w[v], q[v], g.cq[i]); p[v] = fma(s[v], p[v], g.ca[i]); }
     }
+#if !D360_W_FUSED
+#undef w
+#endif
     double s0[VT];
 #pragma unroll
     D360_FORV { s0[v] = w[v] * y2[v]; e2[v] = fma(-s0[v], y2[v], 1.0); }
@@ -294,11 +323,19 @@ __device__ __forceinline__ void project_uv(const FastGroup& g, const double (&tx
     D360_FORV sq[v] = fma(s0[v] * e2[v], fma(e2[v], g.c0375, 0.5), s0[v]);  // sqrt(w) = s0 (1 + e/2 + 3e^2/8)
 #pragma unroll
     D360_FORV {
-        const unsigned hem = (unsigned)__double2hiint(ty[v]) >> 31;  // 1: ty < 0 (sphi > 0)
-        pv[v] = (float)fma(q[v] * sq[v], g.mv[hem], g.cv[hem]);
+        // table slots straight from the sign bytes: a byte permute with sign replication puts
+        // (tx < 0) into byte 0 and (tz < 0) into byte 1, one AND keeps bit 4 of each (byte offsets
+        // 16 OCT_SX and 16 OCT_SZ), the swap adds 16 OCT_SW
         const unsigned hx = (unsigned)__double2hiint(tx[v]), hz = (unsigned)__double2hiint(tz[v]);
-        const unsigned oct = ((hx >> 31) * 2u + (hz >> 31)) * 2u + (swap[v] ? 1u : 0u);
-        pu[v] = (float)fma(fabs(r[v]) * p[v], g.mu[oct], g.cu[oct]);
+        unsigned ko;
+        asm("prmt.b32 %0, %1, %2, 0x44fb;" : "=r"(ko) : "r"(hx), "r"(hz));
+        ko &= 16u * OCT_SX + 16u * OCT_SZ;
+        if (swap[v]) ko |= 16u * OCT_SW;
+        const double2 ut = *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(g.uo) + ko);
+        const unsigned kv = (unsigned)(__double2hiint(ty[v]) >> 31) & 16u;  // 16: ty < 0 (sphi > 0)
+        const double2 vt = *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(g.vo) + kv);
+        pv[v] = (float)fma(q[v] * sq[v], vt.x, vt.y);
+        pu[v] = (float)fma(fabs(r[v]) * p[v], ut.x, ut.y);
     }
 }
 
@@ -410,7 +447,28 @@ __device__ __forceinline__ void accumulate_views_multi(const FastGroup& g, const
     const int half = (ns - 1) / 2;
     const int n_samples = ns * ns;
     const int row_wrap = t.sy - ns * t.sx;
-    const double* rq0 = t.rq + (V0 + vbase) * 3 * t.ne;
+    // views come in (even, odd) pairs that share a z load; a lone view may start anywhere
+    static_assert(NV == 1 || (V0 & 1) == 0, "multi-view passes start at an even view");
+    const double2* rxy0 = t.rxy + (V0 + vbase) * t.ne;
+    const double* rz0 = reinterpret_cast<const double*>(t.rz + ((V0 + vbase) >> 1) * t.ne) + ((V0 + vbase) & 1);
+    auto load_t = [&](int es, double lam, double* tx, double* ty, double* tz) {
+#pragma unroll
+        for (int v = 0; v < NV; v += 2) {
+            if (v + 1 < NV) {
+                const double2 z = *reinterpret_cast<const double2*>(rz0 + 2 * ((v >> 1) * t.ne + es));
+                tz[v] = fma(lam, z.x, rel[v][2]);
+                tz[v + 1] = fma(lam, z.y, rel[v + 1][2]);
+            } else {
+                tz[v] = fma(lam, rz0[2 * ((v >> 1) * t.ne + es)], rel[v][2]);
+            }
+        }
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const double2 xy = rxy0[v * t.ne + es];
+            tx[v] = fma(lam, xy.x, rel[v][0]);
+            ty[v] = fma(lam, xy.y, rel[v][1]);
+        }
+    };
     int e = ce - half * (t.sx + t.sy), col = 0;
     auto next_entry = [&](int cur) {
         int nxt = cur + t.sx;
@@ -430,14 +488,7 @@ __device__ __forceinline__ void accumulate_views_multi(const FastGroup& g, const
             plane_depth(es[j], lam[j], rv[j]);
         }
 #pragma unroll
-        for (int j = 0; j < SPT; ++j) {
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                tx[j * NV + v] = fma(lam[j], rq0[(v * 3 + 0) * t.ne + es[j]], rel[v][0]);
-                ty[j * NV + v] = fma(lam[j], rq0[(v * 3 + 1) * t.ne + es[j]], rel[v][1]);
-                tz[j * NV + v] = fma(lam[j], rq0[(v * 3 + 2) * t.ne + es[j]], rel[v][2]);
-            }
-        }
+        for (int j = 0; j < SPT; ++j) load_t(es[j], lam[j], tx + j * NV, ty + j * NV, tz + j * NV);
         project_uv<SPT * NV>(g, tx, ty, tz, pu, pv);
         gather_bilinear<SPT * NV, NV>(g, nb, g.plane32, pu, pv, val);
 #pragma unroll
@@ -455,12 +506,7 @@ __device__ __forceinline__ void accumulate_views_multi(const FastGroup& g, const
         double lam, rv, tx[NV], ty[NV], tz[NV], val[NV];
         float pu[NV], pv[NV];
         plane_depth(e, lam, rv);
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-            tx[v] = fma(lam, rq0[(v * 3 + 0) * t.ne + e], rel[v][0]);
-            ty[v] = fma(lam, rq0[(v * 3 + 1) * t.ne + e], rel[v][1]);
-            tz[v] = fma(lam, rq0[(v * 3 + 2) * t.ne + e], rel[v][2]);
-        }
+        load_t(e, lam, tx, ty, tz);
         project_uv<NV>(g, tx, ty, tz, pu, pv);
         gather_bilinear<NV>(g, nb, g.plane32, pu, pv, val);
 #pragma unroll
@@ -516,7 +562,7 @@ __device__ __forceinline__ void accumulate_costs(const FastGroup& g, const Tile&
 #pragma unroll
         for (int v = 0; v < NV; ++v) cv[V0 + v] = view_cost<FAST>(g, s0[v], ss0[v], rs0[v], mr, sr);
     } else {
-        constexpr int NA = (NV + 1) / 2;
+        constexpr int NA = 4;  // an even number of views first: the second pass starts at an even view
         accumulate_costs<C, HT, FAST, V0, NA>(g, t, ce, num, nx, ny, nz, mr, sr, bad, cv);
         if (bad) return;
         accumulate_costs<C, HT, FAST, V0 + NA, NV - NA>(g, t, ce, num, nx, ny, nz, mr, sr, bad, cv);

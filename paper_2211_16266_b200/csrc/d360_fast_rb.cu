@@ -88,23 +88,19 @@ __device__ __forceinline__ Tile window_from_stage(const FastGroup& g, unsigned c
     const int wwc = ww / 2;
     const int ne = wwc * hh;
     float4* qg = reinterpret_cast<float4*>(smem);
-    double* rq = reinterpret_cast<double*>(smem + (size_t)ne * sizeof(float4));
+    double2* rxy = reinterpret_cast<double2*>(smem + (size_t)ne * sizeof(float4));
+    double2* rz = rxy + (size_t)C::V * ne;
     for (int e = threadIdx.x; e < ne; e += C::NT) {
         const int j = e / wwc, ic = e - j * wwc;
         const int i = 2 * ic + ((keep + j) & 1);
         const float4 q = stage[j * ww + i];
         qg[e] = q;
-#pragma unroll
-        for (int v = 0; v < C::V; ++v) {
-            const float* r = g.rel_r[v];
-            rq[(v * 3 + 0) * ne + e] = (double)dot3_f32(r[0], r[1], r[2], q.x, q.y, q.z);
-            rq[(v * 3 + 1) * ne + e] = (double)dot3_f32(r[3], r[4], r[5], q.x, q.y, q.z);
-            rq[(v * 3 + 2) * ne + e] = (double)dot3_f32(r[6], r[7], r[8], q.x, q.y, q.z);
-        }
+        store_rq<C>(g, rxy, rz, ne, e, q.x, q.y, q.z);
     }
     Tile t;
     t.qg = qg;
-    t.rq = rq;
+    t.rxy = rxy;
+    t.rz = rz;
     t.wwc = wwc;
     t.ne = ne;
     t.sx = C::stride(g) / 2;
