@@ -37,6 +37,9 @@ constexpr int OCT_SX = 1, OCT_SZ = 16, OCT_SW = 4, OCT_SLOTS = OCT_SX + OCT_SZ +
 #ifndef D360_W_FUSED
 #define D360_W_FUSED 1
 #endif
+#ifndef D360_PIN_C38
+#define D360_PIN_C38 1
+#endif
 #ifndef D360_NT
 #define D360_NT 256  // threads per CTA
 #endif
@@ -265,8 +268,9 @@ __device__ __forceinline__ double rcp3(double x) {
 // max(|tx|,|tz|) = 0, or 1 - |ty|/|t| <= 0); they yield NaN, which the caller maps to `trunc`.
 #define D360_FORV for (int v = 0; v < VT; ++v)
 template <int VT>
-__device__ __forceinline__ void project_uv(const FastGroup& g, const double (&tx)[VT], const double (&ty)[VT],
-                                           const double (&tz)[VT], float (&pu)[VT], float (&pv)[VT]) {
+__device__ __forceinline__ void project_uv(const FastGroup& g, double c38, const double (&tx)[VT],
+                                           const double (&ty)[VT], const double (&tz)[VT], float (&pu)[VT],
+                                           float (&pv)[VT]) {
     double r2[VT], y1[VT], e1[VT], q[VT], w[VT], y2[VT], e2[VT], sq[VT];
 #pragma unroll
     D360_FORV r2[v] = fma(tz[v], tz[v], fma(ty[v], ty[v], fma(tx[v], tx[v], g.tiny)));
@@ -288,7 +292,7 @@ __device__ __forceinline__ void project_uv(const FastGroup& g, const double (&tx
 #pragma unroll
     D360_FORV e3[v] = fma(-hi[v], y3[v], 1.0);
 #pragma unroll
-    D360_FORV y1[v] = fma(y1[v] * e1[v], fma(e1[v], g.c0375, 0.5), y1[v]);
+    D360_FORV y1[v] = fma(y1[v] * e1[v], fma(e1[v], c38, 0.5), y1[v]);
 #pragma unroll
     D360_FORV y3[v] = fma(y3[v], fma(e3[v], e3[v], e3[v]), y3[v]);
     double r[VT], s[VT], p[VT];
@@ -320,7 +324,7 @@ __device__ __forceinline__ void project_uv(const FastGroup& g, const double (&tx
 #pragma unroll
     D360_FORV { s0[v] = w[v] * y2[v]; e2[v] = fma(-s0[v], y2[v], 1.0); }
 #pragma unroll
-    D360_FORV sq[v] = fma(s0[v] * e2[v], fma(e2[v], g.c0375, 0.5), s0[v]);  // sqrt(w) = s0 (1 + e/2 + 3e^2/8)
+    D360_FORV sq[v] = fma(s0[v] * e2[v], fma(e2[v], c38, 0.5), s0[v]);  // sqrt(w) = s0 (1 + e/2 + 3e^2/8)
 #pragma unroll
     D360_FORV {
         // table slots straight from the sign bytes: a byte permute with sign replication puts
@@ -427,22 +431,31 @@ __device__ __forceinline__ void accumulate_views_multi(const FastGroup& g, const
     for (int v = 0; v < NV; ++v)
 #pragma unroll
         for (int c = 0; c < 3; ++c) rel[v][c] = g.rel_t[V0 + vbase + v][c];
-    auto plane_depth = [&](int es, double& lam, double& rv) {
+    // plane depth along the sample's ray (K:241-247): lam, the reference luma, and whether the sample is
+    // poisoned (K:242; the caller ORs it into `bad` when it consumes the sample)
+    auto plane_depth = [&](int es, double& lam, float& rv, bool& par) {
         const float4 q = t.qg[es];
         double dn;
         if constexpr (sizeof(HT) == 4) {
             const float den = dot3_f32(nx, ny, nz, q.x, q.y, q.z);
-            bad = bad || (den > g.den_lim);
+            par = den > g.den_lim;
             dn = (double)fminf(den, g.den_lim);
         } else {
             const double den = fma(nz, (double)q.z, fma(ny, (double)q.y, nx * (double)q.x));
-            const bool par = den > g.neg_par_eps;
-            bad = bad || par;
+            par = den > g.neg_par_eps;
             dn = par ? g.neg_par_eps : den;
         }
         lam = num * rcp3(dn);
-        rv = (double)q.w;
+        rv = q.w;
     };
+    // 3/8 of the third-order rsqrt steps: fma(e, 3/8, 1/2) has two literal operands, one of which has to
+    // sit in a register pair; an opaque move keeps it there for the whole loop instead of two moves per use
+    double c38;
+#if D360_PIN_C38
+    asm volatile("mov.f64 %0, %1;" : "=d"(c38) : "d"(g.c0375));
+#else
+    c38 = g.c0375;
+#endif
     const int ns = C::ns(g);
     const int half = (ns - 1) / 2;
     const int n_samples = ns * ns;
@@ -475,21 +488,38 @@ __device__ __forceinline__ void accumulate_views_multi(const FastGroup& g, const
         if (++col == ns) { col = 0; nxt += row_wrap; }
         return nxt;
     };
+    // The plane-depth chain of a sample (ray load, dot product, reciprocal: a dozen dependent steps with
+    // only SPT-way parallelism) is computed one trip ahead, so that it overlaps the projection and
+    // gather of the samples before it instead of heading every trip.  The last trip prefetches past
+    // the patch: entries inside the CTA's shared memory, values never used.
+    int es[SPT];
+    double lam[SPT];
+    float rvf[SPT];
+    bool par[SPT];
+#pragma unroll
+    for (int j = 0; j < SPT; ++j) {
+        es[j] = e;
+        e = next_entry(e);
+        plane_depth(es[j], lam[j], rvf[j], par[j]);
+    }
     int k = 0;
 #pragma unroll 1
     for (; k + SPT <= n_samples; k += SPT) {
-        int es[SPT];
-        double lam[SPT], rv[SPT], tx[SPT * NV], ty[SPT * NV], tz[SPT * NV], val[SPT * NV];
+        double rv[SPT], tx[SPT * NV], ty[SPT * NV], tz[SPT * NV], val[SPT * NV];
         float pu[SPT * NV], pv[SPT * NV];
+#pragma unroll
+        for (int j = 0; j < SPT; ++j) {
+            load_t(es[j], lam[j], tx + j * NV, ty + j * NV, tz + j * NV);
+            rv[j] = (double)rvf[j];
+            bad = bad || par[j];
+        }
 #pragma unroll
         for (int j = 0; j < SPT; ++j) {
             es[j] = e;
             e = next_entry(e);
-            plane_depth(es[j], lam[j], rv[j]);
+            plane_depth(es[j], lam[j], rvf[j], par[j]);
         }
-#pragma unroll
-        for (int j = 0; j < SPT; ++j) load_t(es[j], lam[j], tx + j * NV, ty + j * NV, tz + j * NV);
-        project_uv<SPT * NV>(g, tx, ty, tz, pu, pv);
+        project_uv<SPT * NV>(g, c38, tx, ty, tz, pu, pv);
         gather_bilinear<SPT * NV, NV>(g, nb, g.plane32, pu, pv, val);
 #pragma unroll
         for (int j = 0; j < SPT; ++j) {
@@ -501,21 +531,24 @@ __device__ __forceinline__ void accumulate_views_multi(const FastGroup& g, const
             }
         }
     }
-#pragma unroll 1
-    for (; k < n_samples; ++k) {
-        double lam, rv, tx[NV], ty[NV], tz[NV], val[NV];
-        float pu[NV], pv[NV];
-        plane_depth(e, lam, rv);
-        load_t(e, lam, tx, ty, tz);
-        project_uv<NV>(g, tx, ty, tz, pu, pv);
-        gather_bilinear<NV>(g, nb, g.plane32, pu, pv, val);
+    // remainder (S not a multiple of SPT): the prefetched samples, one at a time
 #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-            s0[v] += val[v];
-            ss0[v] = fma(val[v], val[v], ss0[v]);
-            rs0[v] = fma(rv, val[v], rs0[v]);
+    for (int j = 0; j < SPT - 1; ++j) {
+        if (k + j < n_samples) {
+            double tx[NV], ty[NV], tz[NV], val[NV];
+            float pu[NV], pv[NV];
+            load_t(es[j], lam[j], tx, ty, tz);
+            const double rv = (double)rvf[j];
+            bad = bad || par[j];
+            project_uv<NV>(g, c38, tx, ty, tz, pu, pv);
+            gather_bilinear<NV>(g, nb, g.plane32, pu, pv, val);
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                s0[v] += val[v];
+                ss0[v] = fma(val[v], val[v], ss0[v]);
+                rs0[v] = fma(rv, val[v], rs0[v]);
+            }
         }
-        e = next_entry(e);
     }
 }
 
