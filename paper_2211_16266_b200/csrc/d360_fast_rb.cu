@@ -110,7 +110,7 @@ __device__ __forceinline__ Tile window_from_stage(const FastGroup& g, unsigned c
 
 template <class C>
 __global__ void __launch_bounds__(C::NT, C::MINB)
-    k_red_black(const __grid_constant__ FastGroup g, const __grid_constant__ WindowMap wm, int parity,
+    k_red_black(const __grid_constant__ FastGroup g, const __grid_constant__ WindowMap wm, int parity_arg,
                 const float* __restrict__ depth_in,
                 const float* __restrict__ normal_in, const float* __restrict__ cost_in, float* __restrict__ depth_out,
                 float* __restrict__ normal_out, float* __restrict__ cost_out,
@@ -118,6 +118,12 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
                 unsigned char* __restrict__ memo_valid, double* __restrict__ memo_cost, unsigned long long* n_evals) {
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr int NT = C::NT;
+    // parity_arg 2: both colours in one launch, one per grid z-slice.  The eight neighbours of a pixel all
+    // have its colour (K:44-56), so the two passes of an iteration read and write disjoint pixels: running
+    // them side by side gives what running them one after the other gives, and the off-colour pixels need
+    // no carrying over (the other slice writes them).
+    const bool both = parity_arg == 2;
+    const int parity = both ? (int)blockIdx.z : parity_arg;
     const int x0 = blockIdx.x * TW, y0 = blockIdx.y * C::TH_RB;  // x0 is even
     const int R = C::reach(g);
     const bool compress = (C::stride(g) & 1) == 0;
@@ -136,7 +142,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
     const int lx = 2 * (tid % (TW / 2)) + ((parity + y) & 1);
     const int x = x0 + lx;
     const bool live = x < g.W && y < g.H;
-    if (y < g.H) {
+    if (y < g.H && !both) {
         // carry the off-colour pixel of this pair over unchanged (E:575-577)
         const int xo = x0 + (lx ^ 1);
         if (xo < g.W) {
@@ -335,7 +341,7 @@ int fast_red_black(const GroupDev& gd, int parity, const float* di, const float*
         const size_t smem = rb_queue_offset(tile_bytes(TW, C::TH_RB, g.reach, (g.stride & 1) == 0, gd.V)) +
                             sizeof(RbQueue<C::NT>);
         if (smem > 200 * 1024) return -1;
-        dim3 grid((gd.W + TW - 1) / TW, (gd.H + C::TH_RB - 1) / C::TH_RB);
+        dim3 grid((gd.W + TW - 1) / TW, (gd.H + C::TH_RB - 1) / C::TH_RB, parity == 2 ? 2 : 1);
         WindowMap wm;
         make_window_map(gd, g.reach, TW, C::TH_RB, &wm);
         auto k = k_red_black<C>;

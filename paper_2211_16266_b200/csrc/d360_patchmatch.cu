@@ -610,15 +610,23 @@ extern "C" int d360_run_patchmatch(const d360_group* g, float* depth, float* nor
         return 1;
     }
     for (int it = 0; it < iterations; ++it) {
-        for (int parity = 0; parity < 2; ++parity) {
-            if (launch_red_black(gd, prec, parity, cd, cn, cc, nd, nn, nc, chg_in, chg_out, memo_valid, memo_cost, n_evals, s))
+        // The two colours never read each other (every neighbour offset of K:44-56 keeps x + y even or
+        // odd), so the throughput kernel takes both passes in one launch; the generic kernels run them
+        // one after the other as the reference does.
+        int frc = -1;
+        if (prec == D360_PREC_MIXED)
+            frc = fast_red_black(gd, 2, cd, cn, cc, nd, nn, nc, chg_in, chg_out, memo_valid, memo_cost, n_evals, s);
+        if (frc > 0) return 1;
+        const int n_pass = frc == 0 ? 1 : 2;
+        for (int parity = 0; parity < n_pass; ++parity) {
+            if (frc != 0 &&
+                launch_red_black(gd, prec, parity, cd, cn, cc, nd, nn, nc, chg_in, chg_out, memo_valid, memo_cost, n_evals, s))
                 return 1;
             float* tmp;
             tmp = cd; cd = nd; nd = tmp;
             tmp = cn; cn = nn; nn = tmp;
             tmp = cc; cc = nc; nc = tmp;
         }
-        // two swaps per iteration: the current state is back in the caller's buffers
         RefineTable tab;
         const float* tb = tables + (size_t)it * 5 * n_cand;
         if (fill_table(&tab, tb, tb + n_cand, tb + 2 * n_cand, tb + 3 * n_cand, tb + 4 * n_cand, n_cand,
@@ -626,6 +634,15 @@ extern "C" int d360_run_patchmatch(const d360_group* g, float* depth, float* nor
             return 1;
         if (launch_refine(gd, prec, tab, cd, cn, cc, chg_out, n_evals, s)) return 1;
         unsigned char* tmpc = chg_in; chg_in = chg_out; chg_out = tmpc;
+    }
+    if (cd != depth) {  // an odd number of buffer swaps: the result goes back to the caller's buffers
+        if (cudaMemcpyAsync(depth, cd, n_px * sizeof(float), cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+            cudaMemcpyAsync(normal, cn, 3 * n_px * sizeof(float), cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+            cudaMemcpyAsync(cost, cc, n_px * sizeof(float), cudaMemcpyDeviceToDevice, s) != cudaSuccess) {
+            set_error("cudaMemcpyAsync(result) failed");
+            return 1;
+        }
+        cc = cost;
     }
     if (valid_out != nullptr) {
         const size_t n = n_px;
