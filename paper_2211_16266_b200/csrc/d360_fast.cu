@@ -2,6 +2,8 @@
 // parameter block.
 #include <string.h>
 
+#include <mutex>
+
 #include "d360_fast.cuh"
 
 namespace d360 {
@@ -22,6 +24,38 @@ static EncodeTiledFn encode_tiled() {
         return reinterpret_cast<EncodeTiledFn>(p);
     }();
     return fn;
+}
+
+namespace {
+struct SmemGrant {
+    const void* kernel;
+    int device;
+    size_t bytes;
+};
+std::mutex g_grant_mutex;
+SmemGrant g_grants[256];
+int g_n_grants = 0;
+}  // namespace
+
+bool smem_already_granted(const void* kernel, size_t smem) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return false;
+    std::lock_guard<std::mutex> lock(g_grant_mutex);
+    for (int i = 0; i < g_n_grants; ++i)
+        if (g_grants[i].kernel == kernel && g_grants[i].device == dev) return g_grants[i].bytes >= smem;
+    return false;
+}
+
+void remember_smem_grant(const void* kernel, size_t smem) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    std::lock_guard<std::mutex> lock(g_grant_mutex);
+    for (int i = 0; i < g_n_grants; ++i)
+        if (g_grants[i].kernel == kernel && g_grants[i].device == dev) {
+            if (g_grants[i].bytes < smem) g_grants[i].bytes = smem;
+            return;
+        }
+    if (g_n_grants < 256) g_grants[g_n_grants++] = SmemGrant{kernel, dev, smem};
 }
 
 void make_window_map(const GroupDev& gd, int reach, int tile_w, int tile_h, WindowMap* wm) {

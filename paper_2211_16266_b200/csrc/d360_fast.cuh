@@ -647,9 +647,6 @@ __device__ __forceinline__ double cand_cost(const FastGroup& g, const Tile& t, i
             double lower = 0.0;
             if (g.top_k >= 2) lower = aggregate<VA>(known, g.top_k - 1) * ((double)(g.top_k - 1) / g.top_k);
             if (g.top_k > 2) lower *= 1.0 - 1e-12;
-#ifdef D360_EXP_NO2ND
-            return lower + 1.0;  // timing experiment only: never run the last view
-#endif
             if (lower >= bound) {  // false for NaN: falls through to the full evaluation
                 if (cuts != nullptr) ++*cuts;
                 return lower;
@@ -704,13 +701,22 @@ bool make_fast_group(const GroupDev& gd, FastGroup* out);
 // no encoder (the kernels then fill the window with plain loads).
 void make_window_map(const GroupDev& gd, int reach, int tile_w, int tile_h, WindowMap* wm);
 
+// Opt a kernel into `smem` bytes of dynamic shared memory.  The attribute is per (kernel, device) and
+// only ever has to grow, so it is set when it first has to and remembered (d360_fast.cu), not before
+// each of the 13 launches of a map.
+bool smem_already_granted(const void* kernel, size_t smem);
+void remember_smem_grant(const void* kernel, size_t smem);
+
 template <typename K>
 static int prepare(K kernel, size_t smem) {
+    const void* key = reinterpret_cast<const void*>(kernel);
+    if (smem_already_granted(key, smem)) return 0;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) {
         set_error("cudaFuncSetAttribute(%zu B smem): %s", smem, cudaGetErrorString(e));
         return 1;
     }
+    remember_smem_grant(key, smem);
     return 0;
 }
 

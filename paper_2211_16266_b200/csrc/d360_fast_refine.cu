@@ -9,69 +9,6 @@ namespace fast {
 // set to 1 where a candidate was accepted, see d360_fast_rb.cu.
 __host__ __device__ inline size_t park_offset(size_t tile) { return (tile + 15) & ~(size_t)15; }
 
-#ifdef D360_REFINE_STATS
-// Experiment only (tools/refine_stats.py): how many refinement evaluations a conservative
-// approximate filter with sample-value error bound delta could reject.  [0] evaluations,
-// [1] accepted, [2] not cut by the V-1 view bound, [3 + i] unresolved at delta_i,
-// [8 + k] evaluations of candidate k, [16 + k] accepts of candidate k.
-__device__ unsigned long long g_refine_stats[96];
-template <class C>
-__device__ __forceinline__ void refine_stats(const FastGroup& g, const Tile& t, int ce, double mr, double sr, double d,
-                                             double nx, double ny, double nz, double bound, int k) {
-    constexpr int VT = C::VT;
-    const float4 a = t.qg[ce];
-    const double ndota = dot3_f64(nx, ny, nz, (double)a.x, (double)a.y, (double)a.z);
-    atomicAdd(&g_refine_stats[0], 1ull);
-    atomicAdd(&g_refine_stats[8 + k], 1ull);
-    if (ndota >= -D360_FACING_EPS || sr < D360_SIGMA_EPS) return;
-    const double num = __dmul_rn(d, ndota);
-    bool bad = false;
-    double s0[VT], ss0[VT], rs0[VT];
-    accumulate_views_multi<C, double, 0, VT, 1>(g, t, ce, num, nx, ny, nz, bad, s0, ss0, rs0);
-    if (bad) return;
-    double cv[VT], sg[VT];
-    for (int v = 0; v < VT; ++v) {
-        cv[v] = view_cost<false>(g, s0[v], ss0[v], rs0[v], mr, sr);
-        const double m0 = s0[v] * g.inv_s;
-        const double v0 = ss0[v] * g.inv_s - m0 * m0;
-        sg[v] = v0 > 0 ? sqrt(v0) : 0.0;
-    }
-    double tmp[VT];
-    for (int v = 0; v < VT; ++v) tmp[v] = cv[v];
-    const double c = aggregate<VT>(tmp, g.top_k);
-    if (c < bound) { atomicAdd(&g_refine_stats[1], 1ull); atomicAdd(&g_refine_stats[16 + k], 1ull); }
-    {
-        const double edges[8] = {0.01, 0.02, 0.05, 0.1, 0.2, 0.5, 1.0, 10.0};
-        int b = 0;
-        while (bound >= edges[b]) ++b;
-        atomicAdd(&g_refine_stats[64 + b], 1ull);
-        double smin = 1e30;
-        for (int v = 0; v < VT; ++v) smin = sg[v] < smin ? sg[v] : smin;
-        const double se[8] = {1e-3, 2e-3, 5e-3, 1e-2, 2e-2, 5e-2, 1e-1, 10.0};
-        b = 0;
-        while (smin >= se[b]) ++b;
-        atomicAdd(&g_refine_stats[72 + b], 1ull);
-    }
-    double mn = 1e30;
-    for (int v = 0; v < VT - 1; ++v) mn = cv[v] < mn ? cv[v] : mn;
-    if (!(0.5 * mn >= bound)) atomicAdd(&g_refine_stats[2], 1ull);
-    const double deltas[5] = {0.0, 1e-5, 3e-5, 1e-4, 3e-4};
-    for (int i = 0; i < 5; ++i) {
-        const double dl = deltas[i];
-        double lb[VT];
-        for (int v = 0; v < VT; ++v) {
-            if (sg[v] > 2 * dl && cv[v] < g.trunc) {
-                const double rho = 1.0 - cv[v];
-                double l = 1.0 - (rho * sg[v] + dl) / (sg[v] - dl);
-                l = l < 0 ? 0 : l;
-                lb[v] = l > g.trunc ? g.trunc : l;
-            } else lb[v] = cv[v] >= g.trunc && dl == 0.0 ? g.trunc : 0.0;
-        }
-        const double L = aggregate<VT>(lb, g.top_k);
-        if (!(L >= bound)) { atomicAdd(&g_refine_stats[3 + i], 1ull); atomicAdd(&g_refine_stats[32 + k * 5 + i], 1ull); }
-    }
-}
-#endif
 
 template <class C>
 __global__ void __launch_bounds__(C::NT, C::MINB)
@@ -140,9 +77,6 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
             if (nrm < 1e-12) continue;
             const double inv = 1.0 / nrm;
             cnx = __dmul_rn(cnx, inv); cny = __dmul_rn(cny, inv); cnz = __dmul_rn(cnz, inv);
-#ifdef D360_REFINE_STATS
-            refine_stats<C>(g, t, ce, mr, sr, nd, cnx, cny, cnz, park[4 * C::NT], k);
-#endif
             const double ev = cand_cost<C, double, true>(g, t, ce, mr, sr, nd, cnx, cny, cnz, park[4 * C::NT], &cuts);
             ++evals;
             if (ev < park[4 * C::NT]) {
@@ -191,16 +125,5 @@ int fast_refine(const GroupDev& gd, const RefineTable& tab, float* depth, float*
     })
     return check_launch("refine_pass");
 }
-
-#ifdef D360_REFINE_STATS
-extern "C" int d360_debug_refine_stats(unsigned long long* out, int reset) {
-    cudaMemcpyFromSymbol(out, d360::fast::g_refine_stats, sizeof(unsigned long long) * 96);
-    if (reset) {
-        unsigned long long z[96] = {0};
-        cudaMemcpyToSymbol(d360::fast::g_refine_stats, z, sizeof(z));
-    }
-    return 0;
-}
-#endif
 
 }  // namespace d360
