@@ -30,13 +30,34 @@ def test_plan_shards_partition_and_halos(n_results, world):
     assert centres == want  # contiguous, ordered, nothing lost or duplicated
     sizes = [len(p.centres) for p in plans]
     assert max(sizes) - min(sizes) <= 1
+    # every depth result is computed exactly once (no halo recompute) ...
+    computed = [i for p in plans for i in p.depth]
+    assert computed == (list(range(n_results)) if want else [])
     for p in plans:
-        for c in p.centres:
+        have_raw = set(p.depth) | set(p.raw_halo)
+        have_filtered = set(p.centres) | set(p.filtered_halo)
+        assert not set(p.depth) & set(p.raw_halo) and not set(p.centres) & set(p.filtered_halo)
+        for c in p.centres:  # ... and what a centre reads is either computed here or received
+            assert all(j in have_raw for j in range(c - 2, c + 3))
             newer = [j for j in range(c + 1, c + buffer) if j < n_results - 2]
-            assert all(j in p.filtered for j in [c, *newer])
-        for f in p.filtered:
-            assert all(j in p.depth for j in range(f - 2, f + 3))
-        assert all(0 <= j < n_results for j in p.depth)
+            assert all(j in have_filtered for j in newer)
+        # halos come from the neighbouring blocks only: at most `half` before, `half` + buffer - 1 after
+        assert len(p.raw_halo) <= 4 and len(p.filtered_halo) <= buffer - 1
+        for f in p.raw_halo:
+            assert any(f in q.depth for q in plans if q.rank != p.rank)
+        for f in p.filtered_halo:
+            assert any(f in q.centres for q in plans if q.rank != p.rank)
+
+
+def test_plan_shards_c5_work_per_rank():
+    """BASELINE config C5 (64 keyframes, 4 neighbours -> 60 depth results) on 8 GPUs: 60 / 8 depth maps
+    per rank, not the 14 of a halo-recompute plan."""
+    from paper_2211_16266_b200.sequence import plan_shards
+
+    plans = plan_shards(60, 8)
+    assert sorted(len(p.depth) for p in plans) == [7, 7, 7, 7, 7, 7, 9, 9]
+    assert sum(len(p.depth) for p in plans) == 60
+    assert max(len(p.raw_halo) + len(p.filtered_halo) for p in plans) <= 7
 
 
 def _fake_batches(plan):
@@ -91,13 +112,94 @@ def test_gather_cloud_gloo_world2(tmp_path, n_results):
     assert list(got["ids"]) == sorted(got["ids"])  # oldest keyframe first
 
 
+class _FakeStage:
+    """Stand-in for DepthStage on a machine without a GPU: frame i is a deterministic pattern."""
+
+    def __init__(self, camera):
+        self.camera, self.device = camera, torch.device("cpu")
+
+
+def _fake_frame(shape, index, salt):
+    g = torch.Generator().manual_seed(1000 * salt + index)
+    return (torch.rand(shape, generator=g, dtype=torch.float32),
+            (torch.rand(shape, generator=g) > 0.5).to(torch.uint8))
+
+
+def _fake_run(plan, n_results, camera):
+    import paper_2211_16266_b200 as p
+    from paper_2211_16266_b200 import pipeline
+    from paper_2211_16266_b200.sequence import ShardRun
+
+    refs = [(100 + i, p.RigidPose(np.eye(3), np.array([0.0, 0.0, 0.1 * i]))) for i in range(n_results)]
+    run = ShardRun([None] * n_results, plan, _FakeStage(camera), pipeline.ConsistencyConfig(), pipeline.FusionConfig(),
+                   refs=refs)
+    for i in plan.depth:
+        run.accept_frame("raw", i, *_fake_frame(camera.shape, i, 1))
+    for c in plan.centres:
+        run.accept_frame("filtered", c, *_fake_frame(camera.shape, c, 2))
+    return run
+
+
+def _halo_worker(rank, world, port, n_results, out_dir):
+    import torch.distributed as dist
+
+    import paper_2211_16266_b200 as p
+    from paper_2211_16266_b200.sequence import exchange_frames, plan_shards
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cam = p.EquirectCamera(16, 8)
+        plans = plan_shards(n_results, world)
+        run = _fake_run(plans[rank], n_results, cam)
+        got = exchange_frames(run, plans, "raw", comm_device="cpu")
+        got += exchange_frames(run, plans, "filtered", comm_device="cpu")
+        frame_bytes = 16 * 8 * 5
+        assert got == frame_bytes * (len(plans[rank].raw_halo) + len(plans[rank].filtered_halo))
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"),
+                 **{f"raw{i}_{k}": t.numpy() for i in plans[rank].raw_halo for k, t in
+                    zip("dv", run.frame_tensors("raw", i))},
+                 **{f"fil{i}_{k}": t.numpy() for i in plans[rank].filtered_halo for k, t in
+                    zip("dv", run.frame_tensors("filtered", i))})
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n_results", [(2, 19), (2, 7), (3, 30)])
+def test_halo_exchange_gloo(tmp_path, world, n_results):
+    """The two point-to-point halo exchanges over a real process group (gloo, CPU tensors): every rank
+    ends up with exactly the frames its plan lists, bit for bit what their owners hold."""
+    import torch.multiprocessing as mp
+
+    import paper_2211_16266_b200 as p
+    from paper_2211_16266_b200.sequence import plan_shards
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mp.spawn(_halo_worker, args=(world, port, n_results, str(tmp_path)), nprocs=world, join=True)
+    cam = p.EquirectCamera(16, 8)
+    plans = plan_shards(n_results, world)
+    assert any(pl.raw_halo for pl in plans) and any(pl.filtered_halo for pl in plans)
+    for pl in plans:
+        z = np.load(tmp_path / f"rank{pl.rank}.npz")
+        for i in pl.raw_halo:
+            d, v = _fake_frame(cam.shape, i, 1)
+            assert np.array_equal(z[f"raw{i}_d"], d.numpy()) and np.array_equal(z[f"raw{i}_v"], v.numpy())
+        for i in pl.filtered_halo:
+            d, v = _fake_frame(cam.shape, i, 2)
+            assert np.array_equal(z[f"fil{i}_d"], d.numpy()) and np.array_equal(z[f"fil{i}_v"], v.numpy())
+
+
 @pytest.mark.gpu
 def test_two_shards_reproduce_single_stream():
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     import paper_2211_16266_b200 as p
     from paper_2211_16266_b200 import engine, pipeline, synth
-    from paper_2211_16266_b200.sequence import densify_shard, gather_cloud, plan_shards
+    from paper_2211_16266_b200.sequence import gather_cloud, simulate_shards
 
     cam = p.EquirectCamera(64, 32)
     scene = synth.default_scene("box")
@@ -113,10 +215,9 @@ def test_two_shards_reproduce_single_stream():
         return pipeline.DepthStage(cam, engine.PatchSpec(), (0.5, 8.0), 2, 0, warp=False)
 
     def run(world):
-        batches = []
-        for plan in plan_shards(len(groups), world):
-            batches += densify_shard(groups, plan, stage(), ccfg, fcfg)
-        return gather_cloud(batches)
+        cloud, runs = simulate_shards(groups, world, stage, ccfg, fcfg)
+        assert sum(r.computed for r in runs) == len(groups)  # every depth map computed once
+        return cloud
 
     one, two, three = run(1), run(2), run(3)
     assert len(one) > 0
@@ -144,14 +245,15 @@ def test_two_shards_reproduce_single_stream():
 
 @pytest.mark.gpu
 def test_c5_sequence_sharding_full_size():
-    """BASELINE config C5: 64 keyframes at 1920x960 with 4 neighbour views, sharded 1 / 8 ways
-    (the 8 shards run one after the other on the one GPU): the gathered cloud is the
-    single-stream cloud bit for bit, oldest keyframe first."""
+    """BASELINE config C5: 64 keyframes at 1920x960 with 4 neighbour views and the C3 settings
+    (6 iterations), sharded 1 / 8 ways (the 8 shards run one after the other on the one GPU, halos
+    handed across): every depth map is computed once and the gathered cloud is the single-stream
+    cloud bit for bit, oldest keyframe first."""
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     import paper_2211_16266_b200 as p
     from paper_2211_16266_b200 import engine, pipeline, synth
-    from paper_2211_16266_b200.sequence import densify_shard, gather_cloud, plan_shards
+    from paper_2211_16266_b200.sequence import simulate_shards
 
     cam = p.EquirectCamera(1920, 960)
     scene = synth.default_scene("corridor")
@@ -165,14 +267,84 @@ def test_c5_sequence_sharding_full_size():
     ccfg, fcfg = pipeline.ConsistencyConfig(), pipeline.FusionConfig()
 
     def run(world):
-        clouds = []
-        for plan in plan_shards(len(groups), world):
-            stage = pipeline.DepthStage(cam, engine.PatchSpec(), (0.5, 16.0), 1, 0, warp=False, init_rng="philox")
-            clouds.append(gather_cloud(densify_shard(groups, plan, stage, ccfg, fcfg)))
-        return pipeline.FusedCloud.concat(clouds)
+        ws = {}
+
+        def stage():  # the simulated ranks share one GPU: one workspace for all of them
+            st = pipeline.DepthStage(cam, engine.PatchSpec(), (0.5, 16.0), 6, 0, warp=False, init_rng="philox")
+            if "ws" in ws:
+                st._ws = ws["ws"]
+            ws["ws"] = st._ws
+            return st
+
+        cloud, runs = simulate_shards(groups, world, stage, ccfg, fcfg)
+        assert [r.computed for r in runs] == [len(r.plan.depth) for r in runs]
+        assert sum(r.computed for r in runs) == len(groups) and max(r.computed for r in runs) <= -(-len(groups) // world) + 2
+        return cloud
 
     one, eight = run(1), run(8)
     assert len(one) > 100000
     assert np.array_equal(one.points, eight.points) and np.array_equal(one.colors, eight.colors)
     assert np.array_equal(one.source_ids, eight.source_ids)
     assert np.all(np.diff(one.source_ids) >= 0)
+
+
+def _nccl_worker(rank, world, port, out_path):
+    import torch.distributed as dist
+
+    import paper_2211_16266_b200 as p
+    from paper_2211_16266_b200 import engine, pipeline, synth
+    from paper_2211_16266_b200.sequence import densify_sequence
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    try:
+        cam, groups = _small_sequence(p, synth)
+        stats = {}
+        cloud, plan = densify_sequence(
+            groups, lambda: pipeline.DepthStage(cam, engine.PatchSpec(), (0.5, 8.0), 2, 0, warp=False, device=dev),
+            pipeline.ConsistencyConfig(), pipeline.FusionConfig(), rank=rank, world=world, stats=stats)
+        assert stats["depth_maps_computed"] == len(plan.depth)
+        if rank == 0:
+            np.savez(out_path, points=cloud.points, colors=cloud.colors, ids=cloud.source_ids)
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def _small_sequence(p, synth):
+    cam = p.EquirectCamera(64, 32)
+    scene = synth.default_scene("box")
+    kfs = []
+    for k in range(13):
+        pose = p.RigidPose(np.eye(3), np.array([0.1, 0.0, -0.6 + 0.1 * k]))
+        img, _ = synth.render_scene(scene, cam, pose)
+        kfs.append(p.Keyframe(id=k, image=img, pose=pose))
+    return cam, [p.StereoGroup(reference=kfs[i], neighbors=(kfs[i - 1], kfs[i + 1]), camera=cam) for i in range(1, 12)]
+
+
+@pytest.mark.gpu
+def test_densify_sequence_nccl_world2(tmp_path):
+    """Two ranks on two GPUs over NCCL: halo send / recv and the all-gather-v of the cloud; the result is
+    the single-process cloud bit for bit.  Needs two visible GPUs (skipped on the 1-GPU boxes)."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs two CUDA devices")
+    import torch.multiprocessing as mp
+
+    import paper_2211_16266_b200 as p
+    from paper_2211_16266_b200 import engine, pipeline, synth
+    from paper_2211_16266_b200.sequence import simulate_shards
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = tmp_path / "cloud.npz"
+    mp.spawn(_nccl_worker, args=(2, port, str(out)), nprocs=2, join=True)
+    got = np.load(out)
+    cam, groups = _small_sequence(p, synth)
+    one, _ = simulate_shards(groups, 1, lambda: pipeline.DepthStage(cam, engine.PatchSpec(), (0.5, 8.0), 2, 0, warp=False),
+                             pipeline.ConsistencyConfig(), pipeline.FusionConfig())
+    assert np.array_equal(got["points"], one.points) and np.array_equal(got["colors"], one.colors)
+    assert np.array_equal(got["ids"], one.source_ids)
