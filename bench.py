@@ -8,17 +8,22 @@ keyframe that enters the sliding window (each keyframe is converted once and reu
 groups it takes part in), plane-map warp from the previous keyframe + random fill,
 eval + I x (red, black, refine) PatchMatch passes, median outlier filter, pole mask, and the
 geometric-consistency filter of the centre frame of the last 5 depth maps (BASELINE.json
-configs[2], "C3").  N > 1: one process per GPU (torchrun), every rank densifies its own
-keyframe sequence, no data-path collective -> weak scaling.
+configs[2], "C3").  N > 1: one process per GPU (torchrun); the ranks share one sequence of N x K
+depth results (BASELINE.json configs[4], "C5", at K keyframes per rank -> weak scaling) through
+paper_2211_16266_b200.sequence.densify_sequence: every rank computes its block of depth maps once,
+exchanges the consistency / fusion halos with its neighbours point to point over NCCL, fuses its
+centres, and the cloud is gathered to rank 0 - all inside the timed region.
 
 Prints ONE JSON line (rank 0).  `value` = keyframes of all ranks / max-over-ranks device
 time with the uint8 frames already resident in HBM; `e2e` = the same through the host-array
 streaming API (numpy frames in pinned memory -> StreamingDensifier.push -> numpy depth + mask)
 with the copies inside the timed region.
 
-`--impl reference` times the CPU restatement of the reference path (oracle/, C + pthreads,
-all host cores) on a bounded sample of the same workload; the product arm never touches it
-except for the `cpu_baseline` leg at N=1.
+`--impl reference` times the CPU path on the box's host cores at the workload's own size: the C
+port of the reference (oracle/, pthreads, all host threads) on full-resolution keyframes with the
+metric's 4 neighbour views, and beside it the unmodified reference itself (baseline/_ref, numba) on
+one keyframe with the 2 neighbours it supports.  Neither leg imports the product package; the
+product arm touches oracle/ only for its `cpu_baseline` leg at N=1 (one full-size keyframe).
 """
 from __future__ import annotations
 
@@ -143,6 +148,49 @@ class ClockSampler:
 # product arm
 # ---------------------------------------------------------------------------------------
 
+def roofline_block(trace, evals, n_cut, S, V, workload, P, iters, maps, dev_ms) -> dict:
+    """`roofline` object of the JSON line for the dominant cost kernel of this rank.
+
+    The reference computes everything after lam = num / dn in float64 (numba type inference,
+    DESIGN.md "Precision"), and the 1e-4 cost parity needs (u, v) to ~1e-10 px, so the binding
+    resource is the FP64 pipe: the denominator is the DFMA peak measured in this run (`frac`);
+    `frac_fp32` is the same work against the FP32-FMA peak SURVEY.md section 8d named."""
+    from paper_2211_16266_b200 import _lib
+
+    F = flops_per_eval(S, V)
+    dominant = max(("red_black", "refine", "eval_costs"), key=lambda k: trace.get(k, (0, 0.0))[1])
+    d_cnt, d_ms = trace[dominant]
+    fp64_peak = float(_lib.load().d360_measure_fma_peak(1, 20000))
+    fp32_peak = float(_lib.load().d360_measure_fma_peak(0, 20000))
+    # refinement evaluations decided after V - 1 views did not do the last view's share of F
+    flops = {k: n * F for k, n in evals.items()}
+    flops["refine"] -= n_cut * (S * 83 + 12)
+    achieved = flops[dominant] / (d_ms * 1e-3) / 1e12
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get(workload, {}).get(dominant)
+    peaks = {}
+    pk = ROOT / "MEASURED_PEAKS.json"
+    if pk.exists():
+        peaks = json.loads(pk.read_text())
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    # algorithmic HBM bytes per map: per pass 20 B/px state read + 20 B/px written, images 4 B/px
+    # per frame per pass (SURVEY.md section 8d) -> (1 + 3 I) passes
+    passes = 1 + 3 * iters
+    alg_bytes = P * (passes * (40 + 4 * (1 + V)) + 12)
+    return {"bound": "fp64", "kernel": dominant, "achieved": round(achieved, 3), "peak": round(fp64_peak, 2),
+            "unit": "TFLOP/s", "frac": round(achieved / fp64_peak, 4), "traffic": traffic,
+            "peak_source": "in-run DFMA microbenchmark (MEASURED_PEAKS.json has no FP64/FP32 figure; "
+                           "profiles/fp_peaks.json keeps the last recorded pair); not HBM- or tensor-bound, see roofline.hbm",
+            "fp32_fma_peak": round(fp32_peak, 2), "frac_fp32": round(achieved / fp32_peak, 4),
+            "flops_per_eval": F, "evals_per_launch": evals[dominant] // max(d_cnt, 1),
+            "flops_per_launch": flops[dominant] // max(d_cnt, 1), "ms_per_launch": round(d_ms / d_cnt, 4),
+            "hbm": {"algorithmic_bytes_per_step": alg_bytes,
+                    "achieved_gbs": round(alg_bytes * maps / (dev_ms * 1e-3) / 1e9, 2), "peak_gbs": hbm_peak,
+                    "frac": round(alg_bytes * maps / (dev_ms * 1e-3) / 1e9 / hbm_peak, 5)}}
+
+
 def run_product(args) -> dict | None:
     import torch
     import torch.distributed as dist
@@ -157,12 +205,25 @@ def run_product(args) -> dict | None:
         if world == 1 and args.gpus > 1:
             raise SystemExit(f"--gpus {args.gpus} needs torchrun (one process per GPU); WORLD_SIZE is 1")
         raise SystemExit(f"--gpus {args.gpus} does not match WORLD_SIZE={world}")
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # D360_BENCH_BACKEND=gloo: rehearsal of the N > 1 path on a box with fewer GPUs than ranks (ranks
+    # share GPUs, halos and cloud staged through host memory); the measured configuration is NCCL
+    backend = os.environ.get("D360_BENCH_BACKEND", "nccl")
+    dev_index = local_rank if backend == "nccl" else local_rank % torch.cuda.device_count()
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "WARN")
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     _lib.load()
+    if world > 1:
+        out = run_product_sharded(args, world, rank, dev, backend)
+        dist.barrier()
+        dist.destroy_process_group()
+        return out
 
     W, H, V, hw, stride, iters = WORKLOADS[args.workload]
     S = n_samples_of(hw, stride)
@@ -337,30 +398,7 @@ def run_product(args) -> dict | None:
         total_traced = sum(ms for _, ms in trace.values())
         for kind, (cnt, ms) in sorted(trace.items(), key=lambda kv: -kv[1][1]):
             kinds[kind] = {"launches": cnt, "ms_per_launch": round(ms / cnt, 4), "share": round(ms / total_traced, 4)}
-        dominant = max(("red_black", "refine", "eval_costs"), key=lambda k: trace.get(k, (0, 0.0))[1])
-        d_cnt, d_ms = trace[dominant]
-        # The reference computes everything after lam = num / dn in float64 (numba type inference,
-        # DESIGN.md "Precision"), and the 1e-4 cost parity needs (u, v) to ~1e-10 px, so the
-        # binding resource is the FP64 pipe: the denominator is the DFMA peak measured in this run.
-        fp64_peak = float(_lib.load().d360_measure_fma_peak(1, 20000))
-        fp32_peak = float(_lib.load().d360_measure_fma_peak(0, 20000))
-        # refinement evaluations decided after V - 1 views did not do the last view's share of F
-        flops = {k: n * F for k, n in evals.items()}
-        flops["refine"] -= n_cut * (S * 83 + 12)
-        achieved = flops[dominant] / (d_ms * 1e-3) / 1e12
-        traffic = None
-        tf = ROOT / "profiles" / "traffic.json"
-        if tf.exists():
-            traffic = json.loads(tf.read_text()).get(args.workload, {}).get(dominant)
-        peaks = {}
-        pk = ROOT / "MEASURED_PEAKS.json"
-        if pk.exists():
-            peaks = json.loads(pk.read_text())
-        hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-        # algorithmic HBM bytes per step: per pass 20 B/px state read + 20 B/px written, images 4 B/px
-        # per frame per pass -> (1 + 3 I) passes
-        passes = 1 + 3 * iters
-        alg_bytes = P * (passes * (40 + 4 * (1 + V)) + 12)
+        roofline = roofline_block(trace, evals, n_cut, S, V, args.workload, P, iters, args.steps, dev_ms)
         result = {
             "metric": METRIC, "value": round(world * args.steps / (dev_ms * 1e-3), 4), "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -378,19 +416,7 @@ def run_product(args) -> dict | None:
                     "h2d_bytes_per_step": bytes_in // args.steps, "d2h_bytes_per_step": bytes_out // args.steps,
                     "ms_per_step": round(e2e_ms / args.steps, 3)},
             "gpu_launches": int(launches),
-            "roofline": {"bound": "fp64", "kernel": dominant, "achieved": round(achieved, 3),
-                         "peak": round(fp64_peak, 2), "unit": "TFLOP/s", "frac": round(achieved / fp64_peak, 4),
-                         "traffic": traffic,
-                         "peak_source": "in-run DFMA microbenchmark (MEASURED_PEAKS.json has no FP64/FP32 figure); "
-                                        "not HBM- or tensor-bound, see roofline.hbm",
-                         "fp32_fma_peak": round(fp32_peak, 2),
-                         "flops_per_eval": F, "evals_per_launch": evals[dominant] // max(d_cnt, 1),
-                         "flops_per_launch": flops[dominant] // max(d_cnt, 1),
-                         "ms_per_launch": round(d_ms / d_cnt, 4),
-                         "hbm": {"algorithmic_bytes_per_step": alg_bytes,
-                                 "achieved_gbs": round(alg_bytes * args.steps / (dev_ms * 1e-3) / 1e9, 2),
-                                 "peak_gbs": hbm_peak,
-                                 "frac": round(alg_bytes * args.steps / (dev_ms * 1e-3) / 1e9 / hbm_peak, 5)}},
+            "roofline": roofline,
             "kernels": kinds,
             "evals_per_step": {k: v // args.steps for k, v in evals.items()},
             "refine_evals_cut_after_v_minus_1_views_per_step": n_cut // args.steps,
@@ -401,67 +427,297 @@ def run_product(args) -> dict | None:
     return result
 
 
+
+def run_product_sharded(args, world: int, rank: int, dev, backend: str) -> dict | None:
+    """N > 1: one sequence of world x steps depth results, sharded by keyframe (sequence.py)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2211_16266_b200 as p
+    from paper_2211_16266_b200 import _lib, engine, pipeline, sequence, synth
+
+    W, H, V, hw, stride, iters = WORKLOADS[args.workload]
+    S = n_samples_of(hw, stride)
+    cam = p.EquirectCamera(W, H)
+    spec = engine.PatchSpec(hw, stride, 1.2)
+    scene = synth.default_scene("box")
+    ccfg, fcfg = pipeline.ConsistencyConfig(), pipeline.FusionConfig()
+    nb_order = []
+    for k in range(1, V // 2 + 1):
+        nb_order += [-k, k]
+    half_v = V // 2
+    n_results = world * args.steps
+    loop = loop_positions(0)
+    n_kf = n_results + 2 * half_v
+
+    def pose_of(j):
+        return p.RigidPose(np.eye(3), loop[j % len(loop)])
+
+    refs = [(i + half_v, pose_of(i + half_v)) for i in range(n_results)]
+    plan = sequence.plan_shards(n_results, world, ccfg.window, fcfg.buffer)[rank]
+    mine = range(max(0, plan.depth.start), min(n_kf, plan.depth.stop + 2 * half_v)) if len(plan.depth) else range(0)
+    dev_imgs, host_imgs = {}, {}
+    for j in mine:  # the keyframes this rank's groups read: resident on the device and in pinned host memory
+        img, _ = synth.render_scene_device(scene, cam, pose_of(j), dev)
+        dev_imgs[j] = img
+        pinned = torch.empty(img.shape, dtype=torch.uint8).pin_memory()
+        pinned.copy_(img)
+        host_imgs[j] = pinned.numpy()
+    torch.cuda.synchronize()
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    comm_device = None if backend == "nccl" else "cpu"
+
+    def barrier():
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+
+    def run(images, stats):
+        """One pass over the whole sequence from `images` (device tensors or pinned host arrays)."""
+        dk_cache, buffers = {}, {}
+
+        def device_keyframe(j):
+            dk = dk_cache.get(j)
+            if dk is None:
+                dk = dk_cache[j] = engine.DeviceKeyframe(images[j], cam, dev)
+                for old in [k for k in dk_cache if k < j - 2 * V]:
+                    del dk_cache[old]
+            return dk
+
+        def group(i):
+            def make():
+                flush_buf.zero_()  # L2 flush between keyframes, inside the timed region
+                c = i + half_v
+                kfs = [p.Keyframe(id=c, image=host_imgs[c], pose=pose_of(c))] + \
+                      [p.Keyframe(id=c + o, image=host_imgs[c + o], pose=pose_of(c + o)) for o in nb_order]
+                g = p.StereoGroup(reference=kfs[0], neighbors=tuple(kfs[1:]), camera=cam)
+                return engine.PreparedGroup(g, spec, precision=args.precision, device=dev, buffers=buffers,
+                                            device_keyframes=[device_keyframe(c)] + [device_keyframe(c + o) for o in nb_order])
+            return make
+
+        groups = [group(i) for i in range(n_results)]
+
+        def stage_factory():
+            st = pipeline.DepthStage(cam, spec, DEPTH_RANGE, iters, SEED, warp=True, precision=args.precision,
+                                     init_rng="philox", device=dev, count_evals=True)
+            stats["stage"] = st
+            return st
+
+        return sequence.densify_sequence(groups, stage_factory, ccfg, fcfg, rank=rank, world=world, refs=refs,
+                                         comm_device=comm_device, stats=stats)
+
+    # warm-up: kernels, allocator, NCCL channels (a short sequence through the same path)
+    warm_stage = pipeline.DepthStage(cam, spec, DEPTH_RANGE, iters, SEED, warp=True, precision=args.precision,
+                                     init_rng="philox", device=dev)
+    if len(plan.depth):
+        for _ in range(args.warmup):
+            c = plan.depth.start + half_v
+            kfs = [p.Keyframe(id=c, image=host_imgs[c], pose=pose_of(c))] + \
+                  [p.Keyframe(id=c + o, image=host_imgs[c + o], pose=pose_of(c + o)) for o in nb_order]
+            warm_stage.process_device(p.StereoGroup(reference=kfs[0], neighbors=tuple(kfs[1:]), camera=cam))
+    del warm_stage
+    tok = torch.zeros(1, device=dev if backend == "nccl" else "cpu")
+    dist.all_reduce(tok)
+    barrier()
+
+    _lib.trace_enable(True)
+    launches0 = _lib.launch_count()
+    stats = {}
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    gc.collect()
+    gc.disable()
+    with ClockSampler(dev.index) as clocks:
+        barrier()
+        e0.record()
+        cloud, _ = run(dev_imgs, stats)
+        e1.record()
+        barrier()
+    gc.enable()
+    dev_ms = e0.elapsed_time(e1)
+    launches = _lib.launch_count() - launches0
+    trace = _lib.trace_summary()
+    _lib.trace_enable(False)
+    n_points = len(cloud) if cloud is not None else 0
+    n_evals_counted, n_cut = (int(x) for x in stats.pop("stage").workspace.n_evals.tolist())
+
+    stats_h = {}
+    gc.collect()
+    gc.disable()
+    barrier()
+    t0 = time.perf_counter()
+    cloud_h, _ = run(host_imgs, stats_h)  # frames from pinned host memory, cloud to host on rank 0
+    stats_h.pop("stage", None)
+    barrier()
+    e2e_s = time.perf_counter() - t0
+    gc.enable()
+    bytes_in = sum(host_imgs[j].nbytes for j in mine)
+    bytes_out = (cloud_h.points.nbytes + cloud_h.colors.nbytes + cloud_h.source_ids.nbytes) if cloud_h is not None else 0
+
+    cdev = dev if backend == "nccl" else torch.device("cpu")
+    times = torch.tensor([dev_ms, e2e_s * 1e3], dtype=torch.float64, device=cdev)
+    dist.all_reduce(times, op=dist.ReduceOp.MAX)
+    sums = torch.tensor([stats["depth_maps_computed"], stats["halo_bytes_received"], bytes_in, bytes_out, launches],
+                        dtype=torch.float64, device=cdev)
+    dist.all_reduce(sums, op=dist.ReduceOp.SUM)
+    dev_ms, e2e_ms = (float(x) for x in times.tolist())
+    computed, halo_bytes, bytes_in, bytes_out, launches = (int(x) for x in sums.tolist())
+    if rank != 0:
+        return None
+    kinds = {}
+    total_traced = sum(ms for _, ms in trace.values()) or 1.0
+    for kind, (cnt, ms) in sorted(trace.items(), key=lambda kv: -kv[1][1]):
+        kinds[kind] = {"launches": cnt, "ms_per_launch": round(ms / cnt, 4), "share": round(ms / total_traced, 4)}
+    mine_n = stats["depth_maps_computed"]  # rank 0's own block
+    P = W * H
+    evals = {"eval_costs": P * mine_n, "refine": 6 * P * iters * mine_n}
+    evals["red_black"] = n_evals_counted - evals["refine"]
+    roofline = roofline_block(trace, evals, n_cut, S, V, args.workload, P, iters, mine_n, dev_ms)
+    return {
+        "metric": METRIC, "value": round(n_results / (dev_ms * 1e-3), 4), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dev_ms / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64/f32 mixed" if args.precision == "mixed" else "f64",
+        "data": "synthetic (GPU-rendered textured box room, value-noise texture)",
+        "config": {"workload": f"c5 at {args.steps} keyframes per GPU: one sequence of {n_results} depth results at {W}x{H}, "
+                               f"{V} neighbour views, {S}-sample {2 * hw + 1}x{2 * hw + 1} patch, {iters} iterations, warp init "
+                               f"(restarted per shard) + median + pole mask + consistency(window 5) + fusion(buffer 4), "
+                               f"keyframe-sharded with halo exchange and cloud gather inside the timed region",
+                   "precision": args.precision, "top_k": engine.default_top_k(V), "init": "warp + philox fill",
+                   "l2": "256 MiB memset between keyframes (inside the timed region); working set > L2",
+                   "keyframes_per_rank": args.steps, "parallelism": f"keyframe-sharded x{world}", "backend": backend,
+                   "depth_maps_computed_all_ranks": computed, "halo_bytes_received_all_ranks": halo_bytes,
+                   "cloud_points": n_points},
+        "clocks": clocks.summary(),
+        "e2e": {"value": round(n_results / (e2e_ms * 1e-3), 4), "unit": UNIT,
+                "h2d_bytes_per_step": bytes_in // max(n_results, 1), "d2h_bytes_per_step": bytes_out // max(n_results, 1),
+                "ms_per_step": round(e2e_ms / args.steps, 3)},
+        "gpu_launches": launches,
+        "roofline": roofline,
+        "kernels_rank0": kinds,
+    }
+
+
 # ---------------------------------------------------------------------------------------
 # CPU arm: the oracle (C restatement of the reference) on a bounded sample
 # ---------------------------------------------------------------------------------------
 
-CPU_SAMPLE = {"c1": (256, 128), "c2": (320, 160), "c3": (384, 192), "c4": (384, 192)}
+REF_ROOT = ROOT / "baseline" / "_ref"  # the unmodified reference, pip-installed (--target) from /root/reference/pkg
 
 
-def render_cpu_inputs(w: int, h: int, n: int):
-    """Frames for the CPU arm.  Rendered with the product's GPU renderer when a GPU is
-    visible (input generation, outside every timed region), else a numpy sinusoid-textured
-    box so the arm also runs on a GPU-less machine."""
-    poses = [(np.eye(3), t) for t in sequence_positions(0)[:n]]
-    try:
-        import torch
+def _reference_on_path() -> bool:
+    """Make the installed reference importable (it is not product code and never imported by it)."""
+    if not (REF_ROOT / "densify360").is_dir():
+        return False
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/d360_numba_cache")
+    if str(REF_ROOT) not in sys.path:
+        sys.path.insert(0, str(REF_ROOT))
+    return True
 
-        if torch.cuda.is_available():
-            import paper_2211_16266_b200 as p
-            from paper_2211_16266_b200 import synth
 
-            cam = p.EquirectCamera(w, h)
-            scene = synth.default_scene("box")
-            return [synth.render_scene(scene, cam, p.RigidPose(r, t))[0] for r, t in poses], poses
-    except Exception:
-        pass
+def _render_one(job):
+    """One frame of the benchmark scene by the reference's own renderer (synth.py:154-169), or, when the
+    reference is not installed, a numpy sinusoid-textured box (same geometry)."""
+    w, h, t, use_ref = job
+    if use_ref:
+        _reference_on_path()
+        from densify360 import geometry as G, synth as SY
+
+        img, _ = SY.render_scene(SY.default_scene("box"), G.EquirectCamera(w, h), G.RigidPose(np.eye(3), np.asarray(t)))
+        return np.ascontiguousarray(img)
     ys, xs = np.mgrid[0:h, 0:w]
     lam = 2 * np.pi * (xs + 0.5) / w - np.pi
     phi = np.pi / 2 - np.pi * (ys + 0.5) / h
     d = np.stack([np.cos(phi) * np.sin(lam), -np.sin(phi), np.cos(phi) * np.cos(lam)], -1)
     half = np.array([2.0, 1.5, 2.5])
-    imgs = []
-    for _, t in poses:
-        with np.errstate(divide="ignore", invalid="ignore"):
-            tt = np.where(d > 0, (half - t) / d, (-half - t) / d)
-        hit = t + d * tt.min(-1, keepdims=True)
-        tex = sum(np.sin(hit @ k + ph) for k, ph in (((7.1, 3.3, 5.9), 0.3), ((13.7, 17.9, 11.3), 1.1),
-                                                      ((29.0, 23.0, 31.0), 2.0)))
-        g = np.clip(127.5 + 40.0 * tex, 0, 255).astype(np.uint8)
-        imgs.append(np.repeat(g[..., None], 3, axis=2))
-    return imgs, poses
+    with np.errstate(divide="ignore", invalid="ignore"):
+        tt = np.where(d > 0, (half - t) / d, (-half - t) / d)
+    hit = t + d * tt.min(-1, keepdims=True)
+    tex = sum(np.sin(hit @ k + ph) for k, ph in (((7.1, 3.3, 5.9), 0.3), ((13.7, 17.9, 11.3), 1.1),
+                                                  ((29.0, 23.0, 31.0), 2.0)))
+    g = np.clip(127.5 + 40.0 * tex, 0, 255).astype(np.uint8)
+    return np.repeat(g[..., None], 3, axis=2)
 
 
-def run_cpu(workload: str, steps: int, warmup: int, max_seconds: float = 240.0) -> dict:
-    """maps/s of the CPU path, measured on a reduced-resolution sample and scaled by pixel count."""
+def render_cpu_inputs(w: int, h: int, indices):
+    """Frames of the product arm's scene for the CPU arm, rendered on the host cores (one process per
+    frame; ~11 s per 1920x960 frame with the reference's renderer) outside every timed region.  The
+    product's GPU renderer reproduces these bytes for identity rotations (tests/test_gpu_parity.py), so
+    both arms see the same images; the product package is not imported here."""
+    import multiprocessing as mp
+
+    use_ref = _reference_on_path()
+    pos = sequence_positions(0)
+    jobs = [(w, h, pos[i], use_ref) for i in indices]
+    with mp.get_context("spawn").Pool(min(len(jobs), os.cpu_count() or 1)) as pool:
+        imgs = pool.map(_render_one, jobs)
+    return dict(zip(indices, imgs)), ("reference synth.render_scene" if use_ref else "numpy sinusoid box")
+
+
+def time_reference_v2(imgs, order, w, h, hw, stride, iters) -> dict | None:
+    """The reference's own numba path (engine.run_patchmatch, E:529-631) on one full-resolution keyframe
+    with its 2 neighbours (the only neighbourhood it accepts, keyframes.py:47-49), all host cores,
+    after a JIT warm-up on a small image."""
+    if not _reference_on_path():
+        return None
+    try:
+        import numba
+        from densify360 import engine as E, geometry as G, keyframes as KF
+    except Exception as exc:  # numba / Pillow missing on this host
+        return {"unavailable": f"{type(exc).__name__}: {exc}"}
+    cores = os.cpu_count() or 1
+    pos = sequence_positions(0)
+
+    def group(cam, i, crop=None):
+        def kf(j):
+            im = imgs[j] if crop is None else np.ascontiguousarray(imgs[j][::crop, ::crop])
+            return KF.Keyframe(id=j, image=im, pose=G.RigidPose(np.eye(3), pos[j]))
+        return KF.StereoGroup(reference=kf(i), neighbors=(kf(i - 1), kf(i + 1)), camera=cam)
+
+    spec = E.PatchSpec(hw, stride, 1.2)
+    small = G.EquirectCamera(w // 8, h // 8)
+    i = order[0]
+    init = E.random_init(E.PlaneMap.empty(small, DEPTH_RANGE), DEPTH_RANGE, SEED + i)
+    E.run_patchmatch(group(small, i, 8), init, spec, 1, SEED + i, workers=cores)  # JIT
+    cam = G.EquirectCamera(w, h)
+    g = group(cam, i)
+    init = E.random_init(E.PlaneMap.empty(cam, DEPTH_RANGE), DEPTH_RANGE, SEED + i)
+    t0 = time.perf_counter()
+    E.run_patchmatch(g, init, spec, iters, SEED + i, workers=cores)
+    dt = time.perf_counter() - t0
+    return {"seconds_per_map": round(dt, 2), "maps_per_s": round(1.0 / dt, 5), "views": 2,
+            "threads": int(numba.get_num_threads()), "what": f"densify360.engine.run_patchmatch {w}x{h}, 2 neighbours, "
+            f"{iters} iterations, random init, numba {numba.__version__}"}
+
+
+def run_cpu(workload: str, steps: int, warmup: int, max_seconds: float = 200.0, with_reference: bool = True) -> dict:
+    """maps/s of the CPU path at the workload's own size and view count: the C port of the reference
+    (oracle/, pthreads over rows, all host threads, -O3 -march=native timing build) runs the same chain
+    as the product arm (warp init + PatchMatch + median + pole mask + consistency) on full-resolution
+    keyframes for as many steps as `max_seconds` allows (at least one timed keyframe, never a scaled
+    crop).  The reference's own numba path is timed beside it on one keyframe with 2 neighbours."""
     from oracle import d360_oracle as O
 
-    O.build()
+    O.use_timing_build()
     cores = os.cpu_count() or 1
     O.set_threads(cores)
     W, H, V, hw, stride, iters = WORKLOADS[workload]
-    w, h = CPU_SAMPLE[workload]
-    imgs, poses = render_cpu_inputs(w, h, SEQ_LEN)
     nb_order = []
     for k in range(1, V // 2 + 1):
         nb_order += [-k, k]
-    order = walk(warmup + steps)
+    order = walk(max(1, warmup) + steps)
+    # the chain visits consecutive keyframes: render only what the affordable steps can reach
+    reach = min(len(order), 2 + int(max_seconds // 8))
+    need = sorted({i + o for i in order[:reach] for o in [0] + nb_order})
+    t_r = time.perf_counter()
+    imgs, renderer = render_cpu_inputs(W, H, need)
+    render_s = time.perf_counter() - t_r
+    poses = {i: (np.eye(3), sequence_positions(0)[i]) for i in need}
     prev = None
     window = deque(maxlen=5)
     spent = []
     t_start = time.perf_counter()
-    done = 0
-    for n, i in enumerate(order):
+    n_warm = 1 if warmup >= 1 else 0  # one untimed keyframe: page-in, thread pool, first warp source
+    for n, i in enumerate(order[:reach]):
         t0 = time.perf_counter()
         g = O.Group(imgs[i], [imgs[i + o] for o in nb_order], poses[i], [poses[i + o] for o in nb_order],
                     hw, stride, 1.2)
@@ -472,18 +728,23 @@ def run_cpu(workload: str, steps: int, warmup: int, max_seconds: float = 240.0) 
             c = window[2]
             O.consistency_filter(c[0], c[1], c[2], [window[j] for j in (0, 1, 3, 4)])
         dt = time.perf_counter() - t0
-        if n >= warmup:
+        if n >= n_warm:
             spent.append(dt)
-            done += 1
-        if time.perf_counter() - t_start > max_seconds and done >= 1:
+        if spent and time.perf_counter() - t_start + dt > max_seconds:
             break
-    per_map_sample = float(np.mean(spent))
-    scale = (W * H) / (w * h)
-    value = 1.0 / (per_map_sample * scale)
-    return {"value": round(value, 5), "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{done} keyframes of the same scene/config at {w}x{h} ({1 / scale:.4f} of the {W}x{H} pixels), "
-                      f"{per_map_sample:.2f} s each on {cores} threads, scaled by pixel count",
-            "seconds_per_sample_step": round(per_map_sample, 3), "steps_done": done}
+        if len(spent) >= steps:
+            break
+    per_map = float(np.mean(spent))
+    out = {"value": round(1.0 / per_map, 5), "unit": UNIT, "cores": cores, "kind": "port",
+           "sample": f"{len(spent)} full-size keyframe(s) of the same scene and config ({W}x{H}, {V} neighbour views, "
+                     f"{iters} iterations, warp init + median + pole mask + consistency), {per_map:.1f} s each on {cores} "
+                     f"threads after {n_warm} untimed one; frames by {renderer} ({render_s:.0f} s, untimed)",
+           "seconds_per_sample_step": round(per_map, 3), "steps_done": len(spent), "warmup_done": n_warm}
+    if with_reference:
+        ref = time_reference_v2(imgs, order, W, H, hw, stride, iters)
+        if ref is not None:
+            out["reference_numba_v2"] = ref
+    return out
 
 
 def run_reference(args) -> dict | None:
@@ -493,15 +754,19 @@ def run_reference(args) -> dict | None:
     W, H, V, hw, stride, iters = WORKLOADS[args.workload]
     S = n_samples_of(hw, stride)
     cpu = run_cpu(args.workload, args.steps, args.warmup)
+    base = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    if "reference_numba_v2" in cpu:
+        base["reference_numba_v2"] = cpu["reference_numba_v2"]
     return {
         "impl": "reference", "metric": METRIC, "value": cpu["value"], "unit": UNIT, "n_gpus": args.gpus,
-        "steps": cpu["steps_done"], "warmup": args.warmup, "ms_per_step": round(1e3 / cpu["value"], 1),
+        "steps": cpu["steps_done"], "warmup": cpu["warmup_done"], "ms_per_step": round(1e3 / cpu["value"], 1),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32 mixed (CPU)",
-        "data": "synthetic (textured box room)",
+        "data": "synthetic (textured box room, value-noise texture)",
         "config": {"workload": f"{args.workload}: {W}x{H} keyframe, {V} neighbour views, {S}-sample "
                                f"{2 * hw + 1}x{2 * hw + 1} patch, {iters} iterations, warp init + median + pole "
-                               f"mask + consistency(window 5)", "top_k": 2 if V > 2 else V},
-        "cpu_baseline": {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                               f"mask + consistency(window 5)", "top_k": 2 if V > 2 else V,
+                   "steps_requested": args.steps, "note": "full-size keyframes until the time budget; `steps` = done"},
+        "cpu_baseline": base,
         "e2e": {"value": cpu["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -524,7 +789,7 @@ def main() -> None:
     else:
         out = run_product(args)
         if out is not None and args.gpus == 1 and not args.no_cpu_baseline:
-            cpu = run_cpu(args.workload, steps=3, warmup=1, max_seconds=60.0)
+            cpu = run_cpu(args.workload, steps=1, warmup=0, max_seconds=30.0, with_reference=False)
             out["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
     if out is not None:
         print(json.dumps(out), flush=True)

@@ -31,6 +31,10 @@ DEFAULT_REFINE_DEPTH_FRACTION = 0.25  # E:30
 POLE_LAT_LIMIT_DEG = 85.0
 
 
+_FAST_LIB_PATH = _HERE / "libd360_oracle_fast.so"
+_timing_build = False
+
+
 def build(force: bool = False) -> Path:
     """Compile the C restatement (gcc, seconds)."""
     src = _HERE / "d360_oracle.c"
@@ -39,14 +43,27 @@ def build(force: bool = False) -> Path:
     return _LIB_PATH
 
 
+def use_timing_build() -> Path:
+    """bench.py's CPU arm only: switch this process to the -O3 -march=native build (compiled here, for
+    this host; FMA contraction allowed like the reference's fastmath numba kernels).  Never used as
+    the checker.  Always rebuilt: the library must match the CPU it runs on."""
+    global _lib, _timing_build
+    subprocess.run(["make", "-C", str(_HERE), "-B", "fast"], check=True, capture_output=True)
+    _timing_build, _lib = True, None
+    return _FAST_LIB_PATH
+
+
 _lib = None
 
 
 def lib():
     global _lib
     if _lib is None:
-        build()
-        _lib = C.CDLL(str(_LIB_PATH))
+        if _timing_build:
+            _lib = C.CDLL(str(_FAST_LIB_PATH))
+        else:
+            build()
+            _lib = C.CDLL(str(_LIB_PATH))
         _lib.d360o_get_threads.restype = C.c_int
     return _lib
 

@@ -82,3 +82,28 @@ def test_no_cpu_fallback_and_no_oracle_import():
     pkg = ROOT / "paper_2211_16266_b200"
     for path in pkg.rglob("*.py"):
         assert "oracle" not in path.read_text().replace("oracle/", ""), f"{path} mentions the oracle"
+
+
+@pytest.mark.parametrize("name", ["hot_64x32_ident", "hot_64x32_rot", "hot_256x128_c1"])
+def test_refinement_draw_tables_equal_the_reference(name):
+    """engine.refinement_draw_tables (host logic, E:495-526) reproduces the tables the reference drew
+    for the golden runs, bit for bit (same PCG64 stream, same draw order, same f32 rounding)."""
+    import numpy as np
+
+    from paper_2211_16266_b200 import engine
+
+    z = np.load(ROOT / "tests" / "golden" / f"{name}.npz")
+    dr = z["depth_range"]
+    got = engine.refinement_draw_tables(int(z["seed"]), int(z["iterations"]), 0.25 * (dr[1] - dr[0]), np.deg2rad(60.0))
+    assert got.dtype == np.float32 and np.array_equal(got, z["tables"])
+
+
+def test_integration_md_group_struct_matches_ctypes_table():
+    """The Group structure printed in INTEGRATION.md (what a maintainer would paste) has the fields of
+    the library's own ctypes table, in order."""
+    from paper_2211_16266_b200 import _lib
+
+    text = (ROOT / "INTEGRATION.md").read_text()
+    block = re.search(r"class Group\(C\.Structure\):.*?_fields_ = \[(.*?)\]\n", text, re.S).group(1)
+    names = re.findall(r'\("(\w+)"', block)
+    assert names == [f[0] for f in _lib.Group._fields_]
