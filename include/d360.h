@@ -38,8 +38,10 @@ extern "C" {
 /* Arithmetic policy of the cost kernels. */
 enum {
     D360_PREC_EXACT = 0, /* literal f64 restatement (IEEE div/sqrt, f64 bilinear + sums) */
-    D360_PREC_MIXED = 1, /* f64 projection with Newton-refined rcp/rsqrt, f32 bilinear  */
-    D360_PREC_FAST = 2   /* reserved: all-f32 projection                                */
+    D360_PREC_MIXED = 1, /* f64 projection with DFMA contraction and Newton-refined rcp/rsqrt
+                            seeds (~1e-18), f64 bilinear + sums: the throughput policy      */
+    D360_PREC_FAST = 2   /* reserved, rejected by every entry point: an all-f32 projection
+                            cannot hold the 1e-4 cost parity        */
 };
 
 /* One stereo group in kernel layout == densify360.engine.PreparedGroup (E:137-156),
@@ -89,6 +91,12 @@ int d360_version(void);
  * events on its stream; d360_trace_summary synchronises them and writes one line per
  * kernel kind, "<kind> <launches> <total_ms>\n", returning the byte count (-1 on error). */
 unsigned long long d360_launch_count(void);
+/* Launches that ran on the generic kernels (csrc/d360_patchmatch.cu, about 2x slower) although the
+ * MIXED policy was requested, because the throughput kernels do not cover the group: irregular sample
+ * pattern, no padded f64 planes (nb64 / pads), a padded plane of 2^23 texels or more, or a patch window
+ * above 200 KB of shared memory.  The first launch of each reason is also reported on stderr (silenced by
+ * the environment variable D360_QUIET_FALLBACK).  The reference has no such split (one numba path). */
+unsigned long long d360_generic_fallbacks(void);
 int d360_trace_enable(int on);
 int d360_trace_summary(char *buf, int cap);
 
@@ -99,7 +107,14 @@ int d360_eval_costs(const d360_group *g, const float *depth, const float *normal
 /* replaces kernels.red_black_pass (K:352-473; callers E:403-420, E:578-595).
  * Unlike the reference the caller need NOT pre-copy in->out: off-parity pixels are
  * copied by the kernel.  n_evals (device, optional, uint64) is incremented by the number
- * of cost evaluations executed (duplicate candidates skipped, K:418-432). */
+ * of cost evaluations executed (duplicate candidates skipped, K:418-432).
+ * Contract on cost_in: it must be the cost of the stored hypothesis (what d360_eval_costs or an
+ * earlier pass wrote), as it always is inside run_patchmatch (E:564).  Under D360_PREC_MIXED the
+ * throughput kernel skips a neighbour equal to the pixel's ORIGINAL hypothesis even after that
+ * hypothesis has been displaced; the reference re-evaluates it and strict `<` rejects it exactly
+ * when cost_in is its true cost.  With stale finite costs the two rules can differ, and n_evals
+ * then counts fewer evaluations than the reference executes.  D360_PREC_EXACT follows K:418-432
+ * to the letter. */
 int d360_red_black_pass(const d360_group *g, int parity, const float *depth_in,
                         const float *normal_in, const float *cost_in, float *depth_out,
                         float *normal_out, float *cost_out, unsigned long long *n_evals,

@@ -45,6 +45,7 @@ _SIGNATURES = {
     "d360_last_error": (C.c_char_p, []),
     "d360_version": (C.c_int, []),
     "d360_launch_count": (C.c_ulonglong, []),
+    "d360_generic_fallbacks": (C.c_ulonglong, []),
     "d360_trace_enable": (C.c_int, [C.c_int]),
     "d360_trace_summary": (C.c_int, [C.c_char_p, C.c_int]),
     "d360_eval_costs": (C.c_int, [C.POINTER(Group), c_void, c_void, c_void, c_void]),
@@ -114,6 +115,11 @@ def load():
 def launch_count() -> int:
     """Kernels launched by libd360 since it was loaded."""
     return int(load().d360_launch_count())
+
+
+def generic_fallbacks() -> int:
+    """Launches that fell off the throughput kernels onto the generic ones (include/d360.h)."""
+    return int(load().d360_generic_fallbacks())
 
 
 def trace_enable(on: bool) -> None:

@@ -31,36 +31,91 @@ static std::atomic<int> g_trace_on{0};
 struct TraceRec {
     const char* kind;
     cudaEvent_t e0, e1;
+    int device;
+    bool closed;  // e1 recorded
 };
 static std::mutex g_trace_mu;
 static std::vector<TraceRec> g_trace;
-static std::vector<cudaEvent_t> g_event_pool;
+static unsigned g_trace_generation = 0;  // bumped whenever g_trace is cleared
+// An event belongs to the device it was created on, so the pool of spare events is per device.
+struct PooledEvent {
+    cudaEvent_t e;
+    int device;
+};
+static std::vector<PooledEvent> g_event_pool;
 
-static cudaEvent_t take_event() {
-    if (!g_event_pool.empty()) {
-        cudaEvent_t e = g_event_pool.back();
-        g_event_pool.pop_back();
-        return e;
+static cudaEvent_t take_event(int device) {
+    for (size_t i = 0; i < g_event_pool.size(); ++i) {
+        if (g_event_pool[i].device == device) {
+            cudaEvent_t e = g_event_pool[i].e;
+            g_event_pool[i] = g_event_pool.back();
+            g_event_pool.pop_back();
+            return e;
+        }
     }
     cudaEvent_t e = nullptr;
-    cudaEventCreate(&e);
+    if (cudaEventCreate(&e) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return nullptr;
+    }
     return e;
 }
 
-TraceScope::TraceScope(const char* kind, cudaStream_t s) : idx_(-1), s_(s) {
+TraceScope::TraceScope(const char* kind, cudaStream_t s) : idx_(-1), gen_(0), s_(s) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if (!g_trace_on.load(std::memory_order_relaxed)) return;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
     std::lock_guard<std::mutex> lk(g_trace_mu);
-    TraceRec r{kind, take_event(), take_event()};
-    cudaEventRecord(r.e0, s_);
+    TraceRec r{kind, take_event(dev), take_event(dev), dev, false};
+    if (r.e0 == nullptr || r.e1 == nullptr || cudaEventRecord(r.e0, s_) != cudaSuccess) {
+        (void)cudaGetLastError();  // the launch itself is not affected; this record is dropped
+        if (r.e0) g_event_pool.push_back(PooledEvent{r.e0, dev});
+        if (r.e1) g_event_pool.push_back(PooledEvent{r.e1, dev});
+        return;
+    }
     g_trace.push_back(r);
     idx_ = (int)g_trace.size() - 1;
+    gen_ = g_trace_generation;
 }
 
 TraceScope::~TraceScope() {
     if (idx_ < 0) return;
     std::lock_guard<std::mutex> lk(g_trace_mu);
-    if (idx_ < (int)g_trace.size()) cudaEventRecord(g_trace[idx_].e1, s_);
+    // the trace may have been cleared (d360_trace_enable) while this scope was open: its slot is gone
+    if (gen_ != g_trace_generation || idx_ >= (int)g_trace.size()) return;
+    if (cudaEventRecord(g_trace[idx_].e1, s_) == cudaSuccess) g_trace[idx_].closed = true;
+    else (void)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
+// Generic-kernel fallbacks.  The throughput kernels (d360_fast_*.cu) cover the MIXED policy on
+// regular sample grids with padded f64 planes; anything else runs on the generic kernels of
+// d360_patchmatch.cu, about 2x slower.  That is never silent: every such launch is counted
+// (d360_generic_fallbacks) and the first one of each reason is reported on stderr.
+// ---------------------------------------------------------------------------------------
+static std::atomic<unsigned long long> g_fallbacks{0};
+static thread_local const char* g_fast_reject = "not applicable";
+static std::mutex g_fallback_mu;
+static std::vector<const char*> g_fallback_seen;
+
+int fast_reject(const char* why) {
+    g_fast_reject = why;
+    return -1;
+}
+
+void note_generic_fallback(const char* kernel, const GroupDev& gd) {
+    g_fallbacks.fetch_add(1, std::memory_order_relaxed);
+    const char* why = g_fast_reject;
+    std::lock_guard<std::mutex> lk(g_fallback_mu);
+    for (const char* seen : g_fallback_seen)
+        if (seen == why) return;
+    g_fallback_seen.push_back(why);
+    if (getenv("D360_QUIET_FALLBACK") == nullptr)
+        fprintf(stderr,
+                "libd360: %s runs on the generic kernels (about 2x slower) for this group (%dx%d, %d views, %d "
+                "samples): %s\n",
+                kernel, gd.W, gd.H, gd.V, gd.S, why);
 }
 
 int check_launch(const char* what) {
@@ -162,14 +217,17 @@ extern "C" const char* d360_last_error(void) { return d360::g_error; }
 
 extern "C" unsigned long long d360_launch_count(void) { return d360::g_launches.load(); }
 
+extern "C" unsigned long long d360_generic_fallbacks(void) { return d360::g_fallbacks.load(); }
+
 extern "C" int d360_trace_enable(int on) {
     using namespace d360;
     std::lock_guard<std::mutex> lk(g_trace_mu);
     for (auto& r : g_trace) {
-        g_event_pool.push_back(r.e0);
-        g_event_pool.push_back(r.e1);
+        g_event_pool.push_back(PooledEvent{r.e0, r.device});
+        g_event_pool.push_back(PooledEvent{r.e1, r.device});
     }
     g_trace.clear();
+    ++g_trace_generation;
     g_trace_on.store(on ? 1 : 0);
     return 0;
 }
@@ -180,6 +238,7 @@ extern "C" int d360_trace_summary(char* buf, int cap) {
     struct Agg { const char* kind; int n; double ms; };
     std::vector<Agg> aggs;
     for (auto& r : g_trace) {
+        if (!r.closed) continue;  // scope still open, or its end could not be recorded
         if (cudaEventSynchronize(r.e1) != cudaSuccess) {
             set_error("trace: event synchronize failed: %s", cudaGetErrorString(cudaGetLastError()));
             return -1;

@@ -46,6 +46,7 @@ public:
     TraceScope& operator=(const TraceScope&) = delete;
 private:
     int idx_;
+    unsigned gen_;
     cudaStream_t s_;
 };
 
@@ -67,6 +68,11 @@ int fast_red_black(const struct GroupDev& gd, int parity, const float* di, const
                    unsigned long long* n_evals, cudaStream_t s);
 int fast_refine(const struct GroupDev& gd, const RefineTable& tab, float* depth, float* normal, float* cost,
                 unsigned char* changed, unsigned long long* n_evals, cudaStream_t s);
+
+// A throughput kernel that does not apply records why and returns -1 (fast_reject); the caller
+// then counts and reports the generic-kernel launch (note_generic_fallback), d360_common.cu.
+int fast_reject(const char* why);
+void note_generic_fallback(const char* kernel, const struct GroupDev& gd);
 
 void set_error(const char* fmt, ...);
 int check_launch(const char* what);

@@ -76,20 +76,28 @@ void make_window_map(const GroupDev& gd, int reach, int tile_w, int tile_h, Wind
     if (rc == CUDA_SUCCESS) wm->pad = p;
 }
 
+static bool no(const char* why) {
+    fast_reject(why);
+    return false;
+}
+
 bool make_fast_group(const GroupDev& gd, FastGroup* out) {
     // regular grid?  S = ns^2, offsets (dx, dy) = stride * (i - half, j - half), dy outer (E:60-65)
     int ns = 1;
     while (ns * ns < gd.S) ++ns;
-    if (ns * ns != gd.S || (ns & 1) == 0) return false;
+    if (ns * ns != gd.S || (ns & 1) == 0) return no("the sample pattern is not a square odd grid");
     const int half = (ns - 1) / 2;
     const int stride = ns > 1 ? gd.dx[1] - gd.dx[0] : 1;
-    if (stride < 1) return false;
+    if (stride < 1) return no("the sample pattern is not a regular grid (E:60-65 order)");
     for (int k = 0; k < gd.S; ++k) {
-        if (gd.dx[k] != (k % ns - half) * stride || gd.dy[k] != (k / ns - half) * stride) return false;
+        if (gd.dx[k] != (k % ns - half) * stride || gd.dy[k] != (k / ns - half) * stride)
+            return no("the sample pattern is not a regular grid (E:60-65 order)");
     }
-    if (gd.nb_pad_x < 1 || gd.nb_pad_y < 1 || gd.nb64 == nullptr) return false;  // needs padded f64 planes
+    if (gd.nb_pad_x < 1 || gd.nb_pad_y < 1 || gd.nb64 == nullptr)  // needs padded f64 planes
+        return no("the group carries no padded f64 {value, dx} neighbour planes (d360_group.nb64, pads >= 1)");
     const long long pitch = gd.W + 2 * gd.nb_pad_x, rows = gd.H + 2 * gd.nb_pad_y;
-    if (pitch * rows >= (1ll << 23)) return false;  // f32 index arithmetic must stay exact
+    if (pitch * rows >= (1ll << 23))  // f32 index arithmetic must stay exact
+        return no("a padded neighbour plane has 2^23 texels or more (beyond 3840x1920)");
     FastGroup& g = *out;
     g.W = gd.W; g.H = gd.H; g.ns = ns; g.stride = stride; g.reach = half * stride; g.top_k = gd.top_k;
     g.pitch = (int)pitch;
@@ -133,7 +141,8 @@ bool make_fast_group(const GroupDev& gd, FastGroup* out) {
     }
     g.vo[1] = make_double2(ls * (double)cw[7], -0.5);                   // ty < 0: sphi > 0
     g.vo[0] = make_double2(-ls * (double)cw[7], D360_PI * ls - 0.5);    // ty > 0: sphi < 0, acos = pi - p (K:131)
-    if ((unsigned long long)(pitch * rows) * (unsigned long long)gd.V >= (1ull << 32)) return false;
+    if ((unsigned long long)(pitch * rows) * (unsigned long long)gd.V >= (1ull << 32))
+        return no("the neighbour planes together hold 2^32 texels or more");
     g.plane32 = (unsigned)(pitch * rows);
     g.neg_par_eps = -D360_PARALLEL_EPS;
     g.tiny = 1e-30;

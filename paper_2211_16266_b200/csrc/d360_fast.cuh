@@ -730,8 +730,11 @@ static int prepare(K kernel, size_t smem) {
         case 2: D360_FAST_GEO(2, __VA_ARGS__) break;                                  \
         case 3: D360_FAST_GEO(3, __VA_ARGS__) break;                                  \
         case 4: D360_FAST_GEO(4, __VA_ARGS__) break;                                  \
+        case 5: D360_FAST_GEO(5, __VA_ARGS__) break;                                  \
         case 6: D360_FAST_GEO(6, __VA_ARGS__) break;                                  \
-        default: return -1;                                                           \
+        case 7: D360_FAST_GEO(7, __VA_ARGS__) break;                                  \
+        case 8: D360_FAST_GEO(8, __VA_ARGS__) break;                                  \
+        default: return fast_reject("view count outside 1..8");                       \
     }
 
 }  // namespace fast

@@ -38,7 +38,7 @@ int fast_eval(const GroupDev& gd, const float* depth, const float* normal, float
     if (!make_fast_group(gd, &g)) return -1;
     D360_FAST_DISPATCH(gd.V, {
         const size_t smem = mbar_offset(tile_bytes(TW, C::TH_FULL, g.reach, false, gd.V)) + 16;
-        if (smem > 200 * 1024) return -1;
+        if (smem > 200 * 1024) return fast_reject("the patch window of a tile needs more than 200 KB of shared memory");
         dim3 grid((gd.W + TW - 1) / TW, (gd.H + C::TH_FULL - 1) / C::TH_FULL);
         WindowMap wm;
         make_window_map(gd, g.reach, TW, C::TH_FULL, &wm);

@@ -340,7 +340,7 @@ int fast_red_black(const GroupDev& gd, int parity, const float* di, const float*
     D360_FAST_DISPATCH(gd.V, {
         const size_t smem = rb_queue_offset(tile_bytes(TW, C::TH_RB, g.reach, (g.stride & 1) == 0, gd.V)) +
                             sizeof(RbQueue<C::NT>);
-        if (smem > 200 * 1024) return -1;
+        if (smem > 200 * 1024) return fast_reject("the patch window of a tile needs more than 200 KB of shared memory");
         dim3 grid((gd.W + TW - 1) / TW, (gd.H + C::TH_RB - 1) / C::TH_RB, parity == 2 ? 2 : 1);
         WindowMap wm;
         make_window_map(gd, g.reach, TW, C::TH_RB, &wm);

@@ -444,6 +444,7 @@ static int launch_eval(const GroupDev& gd, int prec, const float* depth, const f
     if (prec == D360_PREC_MIXED) {
         const int frc = fast_eval(gd, depth, normal, cost_out, s);
         if (frc >= 0) return frc;
+        note_generic_fallback("eval_costs", gd);
     }
     const size_t smem = tile_smem_bytes(TILE_W, TILE_H, gd.reach, gd.V);
     dim3 grid((gd.W + TILE_W - 1) / TILE_W, (gd.H + TILE_H - 1) / TILE_H);
@@ -471,6 +472,7 @@ static int launch_red_black(const GroupDev& gd, int prec, int parity, const floa
         const int frc = fast_red_black(gd, parity, di, ni, ci, dout, nout, cout, changed_in, changed_out, memo_valid,
                                        memo_cost, n_evals, s);
         if (frc >= 0) return frc;
+        note_generic_fallback("red_black_pass", gd);
     }
     if (memo_valid != nullptr && cudaMemsetAsync(memo_valid, 0, (size_t)gd.W * gd.H, s) != cudaSuccess) {
         set_error("cudaMemsetAsync(memo validity) failed");
@@ -500,6 +502,7 @@ static int launch_refine(const GroupDev& gd, int prec, const RefineTable& tab, f
     if (prec == D360_PREC_MIXED) {
         const int frc = fast_refine(gd, tab, depth, normal, cost, changed, n_evals, s);
         if (frc >= 0) return frc;
+        note_generic_fallback("refine_pass", gd);
     }
     if (changed != nullptr && cudaMemsetAsync(changed, 1, (size_t)gd.W * gd.H, s) != cudaSuccess) {
         set_error("cudaMemsetAsync(changed flags) failed");

@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -44,7 +45,12 @@ def _device(device=None) -> torch.device:
         raise BackendError("no CUDA device is visible; this package has no CPU fallback")
     if device is None:
         return torch.device("cuda", torch.cuda.current_device())
-    return torch.device(device)
+    dev = torch.device(device)
+    if dev.type != "cuda":
+        raise BackendError(f"device must be a CUDA device, got {dev}; this package has no CPU fallback")
+    if dev.index is None:  # "cuda" == the current device; tensors report an index, so carry one too
+        dev = torch.device("cuda", torch.cuda.current_device())
+    return dev
 
 
 def _stream() -> int:
@@ -257,7 +263,12 @@ def to_gray_device(image, device=None, out: torch.Tensor | None = None, pad=(0, 
     if out64 is not None and (tuple(out64.shape) != (*shape, 2) or out64.dtype != torch.float64 or
                               not out64.is_contiguous()):
         raise ValueError(f"out64 must be a contiguous float64 {(*shape, 2)} tensor")
-    _lib.check(lib.d360_to_gray_padded(_ptr(img), ch, _ptr(out), _ptr(out64), h, w, px, py, _stream()), "to_gray")
+    for name, t in (("image", img), ("out", out), ("out64", out64)):
+        if t is not None and t.device != dev:
+            raise ValueError(f"{name} lives on {t.device}, the launch device is {dev}")
+    with torch.cuda.device(dev):
+        _lib.check(lib.d360_to_gray_padded(_ptr(img), ch, _ptr(out), _ptr(out64), h, w, px, py, _stream()),
+                   "to_gray")
     return out
 
 
@@ -481,6 +492,9 @@ def evaluate_costs_device(prep: PreparedGroup, pm: DevicePlaneMap) -> None:
 
 def red_black_pass_device(prep: PreparedGroup, parity: int, src: DevicePlaneMap, dst: DevicePlaneMap,
                           n_evals: torch.Tensor | None = None) -> None:
+    """One pass of K:352-473.  ``src.cost`` must hold the true costs of ``src``'s hypotheses (as after
+    ``evaluate_costs_device`` or an earlier pass): the mixed policy's duplicate rule relies on it, see
+    include/d360.h."""
     lib = _lib.load()
     with torch.cuda.device(prep.device):
         _lib.check(lib.d360_red_black_pass(prep.struct, int(parity), _ptr(src.depth), _ptr(src.normal),
@@ -551,8 +565,14 @@ def run_patchmatch_device(prep: PreparedGroup, pm: DevicePlaneMap, iterations: i
                           refine_theta_deg: float = DEFAULT_REFINE_THETA_DEG,
                           refine_depth_fraction: float = DEFAULT_REFINE_DEPTH_FRACTION,
                           workspace: PatchMatchWorkspace | None = None, count_evals: bool = False,
-                          check_valid: bool = True, skip_unchanged: bool = True):
+                          check_valid: bool = True, skip_unchanged: bool = True, probes: bool | None = None):
     """Optimise ``pm`` in place on the device; returns (pm, DeviceDepthPanorama).
+
+    ``probes`` (default: environment variable D360_PROBES=1): the reference's monotonicity spot checks
+    (E:567-570, E:596-598, E:622-624) - the cost at 8 fixed probe pixels is read back after every pass and
+    must not have increased, else AssertionError with the reference's message.  The passes are then
+    enqueued one C-ABI call at a time with a read-back in between (a debugging mode: same results, bit
+    for bit, without the memoised candidate costs and with 1 + 3 x iterations synchronisations).
 
     One C-ABI call (d360_run_patchmatch) enqueues eval + iterations x (red, black, refine).
     With ``count_evals`` the executed propagation/refinement cost evaluations are ADDED to
@@ -572,6 +592,10 @@ def run_patchmatch_device(prep: PreparedGroup, pm: DevicePlaneMap, iterations: i
     tables = refinement_draw_tables(seed, iterations, refine_depth_fraction * (dmax - dmin),
                                     math.radians(refine_theta_deg))
     ws = workspace if workspace is not None else PatchMatchWorkspace(prep.camera, prep.device)
+    if probes is None:
+        probes = os.environ.get("D360_PROBES") == "1"
+    if probes:
+        return _run_patchmatch_probed(prep, pm, iterations, tables, ws, count_evals)
     with torch.cuda.device(prep.device):
         valid = torch.empty(prep.camera.shape, dtype=torch.uint8, device=prep.device)
         _lib.check(lib.d360_run_patchmatch(prep.struct, _ptr(pm.depth), _ptr(pm.normal), _ptr(pm.cost),
@@ -583,6 +607,33 @@ def run_patchmatch_device(prep: PreparedGroup, pm: DevicePlaneMap, iterations: i
                    "run_patchmatch")
     pano = DeviceDepthPanorama(prep.camera, pm.depth.clone(), valid)
     return pm, pano
+
+
+def _run_patchmatch_probed(prep: PreparedGroup, pm: DevicePlaneMap, iterations: int, tables: np.ndarray,
+                           ws: "PatchMatchWorkspace", count_evals: bool):
+    """run_patchmatch pass by pass with the reference's probe-pixel assertions (E:567-624)."""
+    h, w = prep.camera.shape
+    dev = prep.device
+    probe_y = torch.as_tensor(np.linspace(0, h - 1, 8).astype(np.int64), device=dev)
+    probe_x = torch.as_tensor(np.linspace(0, w - 1, 8).astype(np.int64), device=dev)
+    n_evals = ws.n_evals if count_evals else None
+    cur = pm
+    nxt = DevicePlaneMap(pm.camera, ws.depth, ws.normal, ws.cost, pm.valid, pm.depth_range)
+    evaluate_costs_device(prep, cur)
+    for it in range(iterations):
+        for parity in (0, 1):
+            red_black_pass_device(prep, parity, cur, nxt, n_evals)
+            ok = bool((nxt.cost[probe_y, probe_x] <= cur.cost[probe_y, probe_x]).all().item())
+            assert ok, "propagation increased a probe pixel's cost"
+            cur, nxt = nxt, cur
+        before = cur.cost[probe_y, probe_x].clone()
+        refine_pass_device(prep, cur, tables[it], pm.depth_range)
+        ok = bool((cur.cost[probe_y, probe_x] <= before).all().item())
+        assert ok, "refinement increased a probe pixel's cost"
+    if cur is not pm:  # never the case: two swaps per iteration
+        pm.depth.copy_(cur.depth); pm.normal.copy_(cur.normal); pm.cost.copy_(cur.cost)
+    valid = (pm.cost < float(prep.spec.cost_truncation)).to(torch.uint8)
+    return pm, DeviceDepthPanorama(prep.camera, pm.depth.clone(), valid)
 
 
 def run_patchmatch(group, init: PlaneMap, spec: PatchSpec, iterations: int, seed: int, workers: int | None = None,

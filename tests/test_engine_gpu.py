@@ -121,3 +121,28 @@ def test_ground_truth_planes_beat_wrong_depths_and_more_iterations_never_hurt(pk
     few, _ = engine.run_patchmatch(group, init, spec, 2, 4)
     many, _ = engine.run_patchmatch(group, init, spec, 5, 4)
     assert many.cost.mean() <= few.cost.mean()
+
+
+def test_probe_mode_runs_the_reference_monotonicity_checks_and_changes_nothing(pkg, monkeypatch):
+    """E:567-570, E:596-598, E:622-624: eight probe pixels are checked after every pass.  The probed drive
+    (pass by pass, no memo) returns what the single-call drive returns, bit for bit."""
+    p, engine, synth = pkg
+    cam = p.EquirectCamera(128, 64)
+    group, _ = synth.make_group(synth.default_scene("box"), cam, n_views=4)
+    spec = engine.PatchSpec()
+    prep = engine.prepare_group(group, spec)
+    init = engine.random_init(engine.PlaneMap.empty(cam, DEPTH_RANGE), DEPTH_RANGE, seed=5)
+    outs = []
+    for probes in (False, True):
+        pm = engine.DevicePlaneMap.from_host(init)
+        pm, pano = engine.run_patchmatch_device(prep, pm, 3, 11, probes=probes)
+        outs.append((pm.depth.cpu(), pm.normal.cpu(), pm.cost.cpu(), pano.valid.cpu()))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+    # the environment switch selects the same path
+    monkeypatch.setenv("D360_PROBES", "1")
+    called = []
+    real = engine._run_patchmatch_probed
+    monkeypatch.setattr(engine, "_run_patchmatch_probed", lambda *a, **k: called.append(1) or real(*a, **k))
+    engine.run_patchmatch_device(prep, engine.DevicePlaneMap.from_host(init), 1, 11)
+    assert called

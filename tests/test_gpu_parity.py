@@ -242,10 +242,13 @@ def test_unchanged_neighbour_skipping_full_size(pkg):
 
 
 @pytest.mark.parametrize("precision", PRECISIONS)
-@pytest.mark.parametrize("n_views,top_k", [(4, 2), (4, 4), (6, 3), (3, 2), (1, 1)])
+@pytest.mark.parametrize("n_views,top_k", [(4, 2), (4, 4), (6, 3), (3, 2), (1, 1), (5, 2), (7, 3), (8, 4)])
 def test_multi_view_topk_vs_oracle(pkg, oracle, n_views, top_k, precision):
-    """V != 2 is unpinned by the reference; the oracle's per-view generalisation is the yardstick."""
+    """V != 2 is unpinned by the reference; the oracle's per-view generalisation is the yardstick.
+    Every view count 1..8 runs on the throughput kernels under the mixed policy (no generic fallback)."""
     p, engine, _, synth = pkg
+    from paper_2211_16266_b200 import _lib
+    fallbacks0 = _lib.generic_fallbacks()
     cam = p.EquirectCamera(64, 32)
     scene = synth.default_scene("box")
     group, gt = synth.make_group(scene, cam, n_views=n_views, step=0.1)
@@ -278,6 +281,31 @@ def test_multi_view_topk_vs_oracle(pkg, oracle, n_views, top_k, precision):
     # (flipped ties from the red-black step would show up here; none expected at this size)
     got = dst.cost.cpu().numpy()
     assert cost_close(got, rc).mean() >= 0.999
+    if precision == "mixed":
+        assert _lib.generic_fallbacks() == fallbacks0, "a mixed-policy launch fell back to the generic kernels"
+
+
+def test_generic_fallback_is_counted_and_reported(pkg, capfd):
+    """A group the throughput kernels do not cover (dense planes: pads 0, no f64 planes) still runs, on the
+    generic kernels, and that is counted and said on stderr - never silent."""
+    p, engine, _, synth = pkg
+    from paper_2211_16266_b200 import _lib
+    cam = p.EquirectCamera(64, 32)
+    group, gt = synth.make_group(synth.default_scene("box"), cam, n_views=2, step=0.1)
+    spec = engine.PatchSpec(5, 3, 1.2)  # offsets -3, 0, 3: a regular grid; the planes below are what is missing
+    prep = engine.prepare_group(group, spec, precision="mixed")
+    dr = (0.5, 16.0)
+    src = engine.DevicePlaneMap.from_host(engine.random_init(engine.PlaneMap.empty(cam, dr), dr, seed=1))
+    before = _lib.generic_fallbacks()
+    engine.evaluate_costs_device(prep, src)
+    want = src.cost.clone()
+    assert _lib.generic_fallbacks() == before
+    prep._struct.nb64 = 0  # the f32 planes alone: what a caller without d360_to_gray_padded's f64 output passes
+    engine.evaluate_costs_device(prep, src)
+    assert _lib.generic_fallbacks() == before + 1
+    assert "generic kernels" in capfd.readouterr().err
+    # the generic kernel under the mixed policy computes the same costs to the parity tolerance
+    assert cost_close(src.cost.cpu().numpy(), want.cpu().numpy()).all()
 
 
 def test_median_filter_bit_exact(pkg):

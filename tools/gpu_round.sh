@@ -1,13 +1,14 @@
 #!/bin/bash
-# One gpurun call: GPU tests, smoke, bench, launch list, one full ncu capture.  Usage:
-#   gpurun --timeout 1500 -- 'bash tools/gpu_round.sh <tag>'
-tag=${1:-r1}
+# One gpurun call: GPU tests, smoke, bench (both arms), launch list, one full ncu capture at a steady-state step.
+#   gpurun --timeout 2400 -- 'bash tools/gpu_round.sh <tag>'
+tag=${1:-r2}
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi_$tag.txt
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu_$tag.log 2>&1; echo "pytest rc=$?"
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu_$tag.log 2>&1; echo "pytest rc=$?"
 tail -3 gpurun_out/pytest_gpu_$tag.log
 timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke_$tag.log 2>&1; echo "smoke rc=$?"; tail -2 gpurun_out/smoke_$tag.log
 timeout 600 python bench.py > gpurun_out/bench_$tag.json 2> gpurun_out/bench_$tag.err; echo "bench rc=$?"; cat gpurun_out/bench_$tag.json; tail -3 gpurun_out/bench_$tag.err
+timeout 600 python bench.py --impl reference > gpurun_out/bench_ref_$tag.json 2> gpurun_out/bench_ref_$tag.err; echo "bench ref rc=$?"; cat gpurun_out/bench_ref_$tag.json; tail -3 gpurun_out/bench_ref_$tag.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$tag.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/bench_under_ncu_$tag.log 2>&1; echo "ncu launches rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_red_black|k_refine" -s 4 -c 2 -o gpurun_out/prof_$tag python tools/profile_c3.py mixed 2 > gpurun_out/ncu_full_$tag.log 2>&1; echo "ncu full rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_red_black|k_refine" -s 27 -c 2 -o gpurun_out/chain_$tag -f python tools/profile_chain.py 3 > gpurun_out/chain_$tag.log 2>&1; echo "ncu full rc=$?"
 ls -la gpurun_out
