@@ -354,14 +354,26 @@ class StreamingDensifier:
 
     Each keyframe is uploaded and converted once; depth maps stay in HBM between stages.  Per
     ``push`` the host traffic is one uint8 frame in and (once the windows are full) one filtered
-    depth map + mask out."""
+    depth map + mask out.
+
+    ``overlap=True`` takes both copies off the compute stream (the reference overlaps its stages with
+    threads and bounded queues; here the stages are CUDA streams and events): the frame goes
+    through a pinned staging buffer and an asynchronous copy on a copy stream that the compute stream
+    waits for by event, and the finished depth map + mask are copied into pinned buffers on the copy
+    stream after an event of the compute stream.  ``push`` then hands out the output of the PREVIOUS
+    finished keyframe (its copy is long complete), so the host never waits for the GPU step it has just
+    enqueued and the next step's kernels queue up behind the running ones; ``drain()`` returns the last
+    output.  Same kernels in the same order on one compute stream: outputs are bit-identical to
+    ``overlap=False``.  (With fusion enabled every fused batch still reads its point count back, which
+    synchronises; the overlap then only covers the copies.)"""
 
     def __init__(self, camera: EquirectCamera, spec: PatchSpec, depth_range, iterations: int, seed: int,
                  n_neighbors: int = 2, warp: bool = True, consistency: ConsistencyConfig | None = None,
                  fusion: FusionConfig | None = None, median_window: int = 5, median_rel_threshold: float = 0.2,
                  top_k: int | None = None, precision: str | None = None, init_rng: str = "pcg64", device=None,
-                 count_evals: bool = False):
+                 count_evals: bool = False, overlap: bool = False):
         self.camera = camera
+        self.overlap = bool(overlap)
         self.order = neighbor_order(n_neighbors)
         self.consistency = consistency if consistency is not None else ConsistencyConfig()
         self.stage = DepthStage(camera, spec, depth_range, iterations, seed, warp=warp, median_window=median_window,
@@ -375,6 +387,69 @@ class StreamingDensifier:
         self._group_buffers = {}  # planes of the group in flight, reused from push to push
         self.jobs = 0       # depth jobs run so far
         self._images = {}   # host image of every reference whose output is still pending (<= window entries)
+        self._pending: deque = deque()  # overlap mode: (copy-done event, StreamOutput fields, pinned depth, pinned mask)
+        if self.overlap:
+            with torch.cuda.device(self.device):
+                self._copy_stream = torch.cuda.Stream(self.device)
+            self._stage_in = []   # two pinned uint8 frames + the event of the last copy out of each
+            self._stage_out = []  # three pinned (depth, mask) pairs, rotated
+            self._n_in = self._n_out = 0
+
+    def _upload(self, image: np.ndarray) -> torch.Tensor:
+        """Host frame -> device through a pinned staging buffer and the copy stream."""
+        image = np.ascontiguousarray(image, dtype=np.uint8)
+        if len(self._stage_in) < 2:
+            self._stage_in.append([torch.empty(image.shape, dtype=torch.uint8).pin_memory(), None])
+        slot = self._stage_in[self._n_in % 2]
+        self._n_in += 1
+        if tuple(slot[0].shape) != image.shape:
+            slot[0], slot[1] = torch.empty(image.shape, dtype=torch.uint8).pin_memory(), None
+        if slot[1] is not None:
+            slot[1].synchronize()  # the copy that last read this buffer (two pushes ago)
+        slot[0].numpy()[...] = image
+        compute = torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(self._copy_stream):
+            dev_img = slot[0].to(self.device, non_blocking=True)
+            slot[1] = torch.cuda.Event()
+            slot[1].record(self._copy_stream)
+        compute.wait_event(slot[1])
+        dev_img.record_stream(compute)
+        return dev_img
+
+    def _download_async(self, pano: DeviceDepthPanorama):
+        """Enqueue depth + mask -> pinned host buffers on the copy stream; returns (event, depth, mask)."""
+        if len(self._stage_out) < 3:
+            h, w = self.camera.shape
+            self._stage_out.append((torch.empty((h, w), dtype=torch.float32).pin_memory(),
+                                    torch.empty((h, w), dtype=torch.uint8).pin_memory()))
+        hd, hv = self._stage_out[self._n_out % 3]
+        self._n_out += 1
+        compute = torch.cuda.current_stream(self.device)
+        ready = torch.cuda.Event()
+        ready.record(compute)
+        with torch.cuda.stream(self._copy_stream):
+            self._copy_stream.wait_event(ready)
+            hd.copy_(pano.depth, non_blocking=True)
+            hv.copy_(pano.valid, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(self._copy_stream)
+        pano.depth.record_stream(self._copy_stream)
+        pano.valid.record_stream(self._copy_stream)
+        return done, hd, hv
+
+    def _collect(self, keep: int) -> list:
+        """Outputs whose copies are complete, oldest first, leaving the `keep` newest in flight."""
+        outs = []
+        while len(self._pending) > keep:
+            done, out, hd, hv = self._pending.popleft()
+            done.synchronize()
+            out.pano = DepthPanorama(self.camera, hd.numpy().copy(), hv.numpy().astype(bool))
+            outs.append(out)
+        return outs
+
+    def drain(self) -> list:
+        """Overlap mode: the outputs still in flight (at most one); empty otherwise."""
+        return self._collect(0)
 
     def push(self, keyframe: Keyframe) -> list:
         """Feed the next keyframe (ids strictly increasing); returns the outputs that
@@ -385,7 +460,11 @@ class StreamingDensifier:
             raise OrderingError(f"keyframe id {keyframe.id} arrived after id {self._last_id}; "
                                 "ids must be strictly increasing")
         self._last_id = keyframe.id
-        self._frames.append((keyframe, DeviceKeyframe(keyframe.image, self.camera, self.device)))
+        image = keyframe.image
+        if self.overlap and not isinstance(image, torch.Tensor):
+            with torch.cuda.device(self.device):
+                image = self._upload(np.asarray(image))
+        self._frames.append((keyframe, DeviceKeyframe(image, self.camera, self.device)))
         if len(self._frames) < self._frames.maxlen:
             return []
         mid = len(self._frames) // 2
@@ -408,11 +487,20 @@ class StreamingDensifier:
         self._window.popleft()
         for old in [k for k in self._images if k < target.id]:
             del self._images[old]  # references the consistency window left behind without an output
-        out = StreamOutput(target.id, pano.to_host(), target.pose, image=self._images.pop(target.id, None))
+        if not self.overlap:
+            out = StreamOutput(target.id, pano.to_host(), target.pose, image=self._images.pop(target.id, None))
+            if self._fusion is not None:
+                batch = self._fusion.push_device(DeviceDepthResult(target.id, pano, target.pose, target.image))
+                out.cloud = None if batch is None else batch.to_host()
+            return [out]
+        with torch.cuda.device(self.device):
+            done, hd, hv = self._download_async(pano)
+        out = StreamOutput(target.id, None, target.pose, image=self._images.pop(target.id, None))
         if self._fusion is not None:
             batch = self._fusion.push_device(DeviceDepthResult(target.id, pano, target.pose, target.image))
             out.cloud = None if batch is None else batch.to_host()
-        return [out]
+        self._pending.append((done, out, hd, hv))
+        return self._collect(1)
 
     def finish(self) -> list:
         """Flush the fusion FIFO; frames still inside the consistency window are

@@ -606,6 +606,44 @@ def test_streaming_densifier_matches_stagewise(pkg):
     assert n_out == len(kfs) - 4 - 4
 
 
+@pytest.mark.parametrize("fusion", [False, True])
+def test_streaming_overlap_mode_is_bit_identical(pkg, fusion):
+    """overlap=True (pinned staging, copy stream, events between the stages, P:489-540's overlap on CUDA
+    streams): the same outputs, bit for bit, one push later, and drain() hands out the last one."""
+    p, engine, pipeline, synth = pkg
+    cam = p.EquirectCamera(64, 32)
+    scene = synth.default_scene("box")
+    kfs = []
+    for k in range(14):
+        pose = p.RigidPose(np.eye(3), np.array([0.05, 0.0, -0.65 + 0.1 * k]))
+        img, _ = synth.render_scene(scene, cam, pose)
+        kfs.append(p.Keyframe(id=k, image=img, pose=pose))
+    spec, dr = engine.PatchSpec(), (0.5, 8.0)
+    runs = {}
+    for overlap in (False, True):
+        sd = pipeline.StreamingDensifier(cam, spec, dr, 2, 3, n_neighbors=4, warp=True,
+                                         fusion=pipeline.FusionConfig() if fusion else None, overlap=overlap)
+        per_push = [sd.push(kf) for kf in kfs]
+        runs[overlap] = (per_push, sd.drain(), sd.finish())
+    plain, late = runs[False], runs[True]
+    assert plain[1] == []
+    flat_plain = [o for outs in plain[0] for o in outs]
+    flat_late = [o for outs in late[0] for o in outs] + late[1]
+    assert [o.id for o in flat_plain] == [o.id for o in flat_late] and len(flat_plain) == 14 - 4 - 4
+    first_plain = next(i for i, outs in enumerate(plain[0]) if outs)
+    first_late = next(i for i, outs in enumerate(late[0]) if outs)
+    assert first_late == first_plain + 1 and len(late[1]) == 1
+    for a, b in zip(flat_plain, flat_late):
+        assert np.array_equal(a.pano.depth, b.pano.depth) and np.array_equal(a.pano.valid, b.pano.valid)
+        assert np.array_equal(a.image, b.image)
+        assert (a.cloud is None) == (b.cloud is None)
+        if a.cloud is not None:
+            assert np.array_equal(a.cloud.points, b.cloud.points) and np.array_equal(a.cloud.colors, b.cloud.colors)
+    assert len(plain[2]) == len(late[2])
+    for a, b in zip(plain[2], late[2]):
+        assert np.array_equal(a.points, b.points)
+
+
 def test_run_patchmatch_end_to_end_v4_topk_vs_oracle(pkg, oracle):
     """V = 4, top-k = 2 (unpinned by the reference; the oracle's per-view generalisation is the
     yardstick): whole run from injected PCG64 hypotheses, statistical end-to-end gate."""
