@@ -1,6 +1,7 @@
 """In-tree build of libd360.so (nvcc, sm_100a).  Cross-compiles without a GPU."""
 from __future__ import annotations
 
+import hashlib
 import os
 import shutil
 import subprocess
@@ -23,12 +24,23 @@ def _nvcc() -> str:
     raise RuntimeError("nvcc not found; cannot build libd360.so")
 
 
+STAMP = PKG / "build" / "libd360.stamp"
+
+
+def source_digest() -> str:
+    """Content hash of every source, header and flag the library is built from.  (A time-stamp
+    comparison would reuse a stale prebuilt library whose file happens to be newer than the sources.)"""
+    h = hashlib.sha256(" ".join(NVCC_FLAGS).encode())
+    for dep in [CSRC / s for s in SOURCES] + HEADERS:
+        h.update(dep.name.encode())
+        h.update(dep.read_bytes())
+    return h.hexdigest()
+
+
 def needs_build() -> bool:
-    if not LIB.exists():
+    if not LIB.exists() or not STAMP.exists():
         return True
-    stamp = LIB.stat().st_mtime
-    deps = [CSRC / s for s in SOURCES] + HEADERS
-    return any(d.stat().st_mtime > stamp for d in deps)
+    return STAMP.read_text().strip() != source_digest()
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
@@ -58,6 +70,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     res = subprocess.run(link, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")
+    STAMP.write_text(source_digest() + "\n")
     return LIB
 
 
