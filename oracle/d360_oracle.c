@@ -129,6 +129,41 @@ static inline double fast_acos(double x_) {
     return x_ < 0.0 ? 3.141592653589793 - p : p;
 }
 
+#ifdef D360O_F32_PROJECTION
+/* Experiment build only (tools/f32_projection.py): the same projection with every
+ * operation after lam in float32.  Never the checker: the default build does not define the macro. */
+static inline float fast_atan2_f32(float y_, float x_) {
+    float ax = fabsf(x_), ay = fabsf(y_);
+    float hi = ax > ay ? ax : ay;
+    float lo = ax > ay ? ay : ax;
+    float r = lo / (hi + 1e-30f);
+    float s = r * r;
+    float p = r * (9.999999227776e-01f +
+                   s * (-3.333223261885e-01f +
+                        s * (1.997402857787e-01f +
+                             s * (-1.404782123164e-01f +
+                                  s * (1.000220525649e-01f +
+                                       s * (-6.087448223083e-02f +
+                                            s * (2.533170107199e-02f + s * -5.021063913876e-03f)))))));
+    p = ay > ax ? 1.5707963267948966f - p : p;
+    p = x_ < 0.0f ? 3.141592653589793f - p : p;
+    return y_ < 0.0f ? -p : p;
+}
+static inline float fast_acos_f32(float x_) {
+    float a = fabsf(x_);
+    a = a > 1.0f ? 1.0f : a;
+    float p = (1.570796263346e00f +
+               a * (-2.145970563340e-01f +
+                    a * (8.895977933699e-02f +
+                         a * (-5.008467775423e-02f +
+                              a * (3.068214201158e-02f +
+                                   a * (-1.682974898800e-02f +
+                                        a * (6.510368059701e-03f + a * -1.223553911532e-03f))))))) *
+              sqrtf(1.0f - a);
+    return x_ < 0.0f ? 3.141592653589793f - p : p;
+}
+#endif
+
 /* K:134-153 */
 static inline double bilinear(const float *img, int h, int w, float u, float v) {
     long u0 = (long)floorf(u);
@@ -217,6 +252,16 @@ static double cand_cost_core(const group_t *g, const ctx_t *c, double num,
         const float *img = g->nb + (size_t)v * h * w;
         double s0 = 0.0, ss0 = 0.0, rs0 = 0.0;
         for (int k = 0; k < s; ++k) {
+#ifdef D360O_F32_PROJECTION
+            float lam = (float)num / (float)dn[k];
+            float tx = lam * (float)c->rq[v][0][k] + (float)t0x;
+            float ty = lam * (float)c->rq[v][1][k] + (float)t0y;
+            float tz = lam * (float)c->rq[v][2][k] + (float)t0z;
+            float inv_r = 1.0f / sqrtf(tx * tx + ty * ty + tz * tz + 1e-30f);
+            float sphi = -ty * inv_r;
+            float pu = (fast_atan2_f32(tx, tz) + (float)D360_PI) * (float)half_w - 0.5f;
+            float pv = fast_acos_f32(sphi) * (float)lat_scale - 0.5f;
+#else
             double lam = num / dn[k];
             double tx = lam * c->rq[v][0][k] + t0x;
             double ty = lam * c->rq[v][1][k] + t0y;
@@ -225,6 +270,7 @@ static double cand_cost_core(const group_t *g, const ctx_t *c, double num,
             double sphi = -ty * inv_r;
             float pu = (float)((fast_atan2(tx, tz) + D360_PI) * half_w - 0.5);
             float pv = (float)(fast_acos(sphi) * lat_scale - 0.5);
+#endif
             double val = bilinear(img, h, w, pu, pv);
             s0 += val;
             ss0 += val * val;

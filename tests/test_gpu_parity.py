@@ -423,10 +423,10 @@ def test_depth_stage_chain_vs_reference(pkg):
     for j, k in enumerate(int(i) for i in z["stage_ids"]):
         res = stage.process(p.StereoGroup(reference=kfs[k], neighbors=(kfs[k - 1], kfs[k + 1]), camera=cam))
         assert res.id == k
-        assert (res.pano.valid == z["stage_valid"][j]).mean() >= 0.99
+        assert (res.pano.valid == z["stage_valid"][j]).mean() >= 0.995  # north_star's bar, on every map
         both = res.pano.valid & z["stage_valid"][j]
         rel = np.abs(res.pano.depth - z["stage_depth"][j])[both] / z["stage_depth"][j][both]
-        assert (rel <= 0.005).mean() >= 0.99
+        assert (rel <= 0.005).mean() >= 0.995
         assert not res.pano.valid[0].any() and not res.pano.valid[-1].any()  # pole rows
 
 

@@ -45,6 +45,54 @@ def test_view_filter_and_keyframe_buffer_match_reference_decisions():
     assert abs(offline.triangulation_angle(np.zeros(3), [1, 0, 0], [0, 1, 0]) - 90.0) < 1e-12
 
 
+def _chain_agreement(got: dict, z) -> tuple:
+    """(mask agreement, depths within 0.5 %) per output keyframe against the reference's own run."""
+    agree, close = [], []
+    for j, kid in enumerate(z["depth_ids"].tolist()):
+        depth, valid = got[kid]
+        agree.append(float((valid == z["valids"][j]).mean()))
+        both = valid & z["valids"][j]
+        close.append(float((np.abs(depth - z["depths"][j])[both] <= 0.005 * z["depths"][j][both]).mean()))
+    return agree, close
+
+
+def oracle_chain(z) -> dict:
+    """The reference's run_offline stages on the CPU oracle: accepted keyframes -> triples ->
+    DepthStage with warp carry-over -> consistency window 5.  {keyframe id: (depth, surviving mask)}."""
+    from oracle import d360_oracle as O
+
+    imgs, rot, tr = z["images"], z["rotations"], z["translations"]
+    accepted = [k for k, d in enumerate(z["decisions"]) if d[0]]
+    dr = (0.5, 8.0)
+    prev, window, out = None, [], {}
+    for a, k, b in zip(accepted, accepted[1:], accepted[2:]):
+        g = O.Group(imgs[k], [imgs[a], imgs[b]], (rot[k], tr[k]), [(rot[a], tr[a]), (rot[b], tr[b])])
+        plane, depth, valid = O.depth_stage(g, k, dr, 4, 0, prev, (rot[k], tr[k]))
+        prev = (*plane, (rot[k], tr[k]))
+        window.append((k, depth, valid, (rot[k], tr[k])))
+        if len(window) == 5:
+            ck, cd, cv, cp = window[2]
+            others = [(d_, v_, p_) for j, (_, d_, v_, p_) in enumerate(window) if j != 2]
+            out[ck] = (cd, O.consistency_filter(cd, cv, cp, others, 2, 0.05))
+            window.pop(0)
+    return out
+
+
+def test_oracle_chain_anchors_the_statistical_gate():
+    """PatchMatch trajectories are chaotic at near-ties: over a 17-job warp-chained run a single
+    flipped tie propagates through the warp carry-over.  The CPU oracle - which reproduces every single pass of
+    the reference to <= 3e-6 under injected state (test_oracle_golden.py) - agrees with the reference's own run
+    of this chain on 99.88 % of the mask pixels and has 99.89 % of the depths within 0.5 % (worst keyframe
+    99.46 %): north_star's 99.5 % bar, met on average, with the compiled-C-vs-numba-fastmath rounding
+    differences as the only cause.  The GPU test below holds the product to the same figures."""
+    z = load_golden("offline_64x32")
+    got = oracle_chain(z)
+    assert sorted(got) == z["depth_ids"].tolist()
+    agree, close = _chain_agreement(got, z)
+    assert np.mean(agree) >= 0.995 and np.mean(close) >= 0.995, (np.mean(agree), np.mean(close))
+    assert min(agree) >= 0.99 and min(close) >= 0.99, (agree, close)
+
+
 @pytest.mark.gpu
 def test_run_offline_matches_reference_run():
     torch = pytest.importorskip("torch")
@@ -64,7 +112,8 @@ def test_run_offline_matches_reference_run():
     for key in ("keyframes_total", "keyframes_accepted", "depth_jobs"):
         assert rep[key] == int(z[key]), key
     assert sorted(res.depths) == z["depth_ids"].tolist()
-    # PatchMatch trajectories are chaotic at near-ties: statistical parity of the maps
+    # PatchMatch trajectories are chaotic at near-ties: statistical parity of the maps, at the
+    # level the CPU oracle itself reaches against the reference on this chain (test above)
     agree, close = [], []
     for j, kid in enumerate(sorted(res.depths)):
         dr = res.depths[kid]
@@ -72,7 +121,15 @@ def test_run_offline_matches_reference_run():
         both = dr.pano.valid & z["valids"][j]
         close.append((np.abs(dr.pano.depth - z["depths"][j])[both] <= 0.005 * z["depths"][j][both]).mean())
         assert not dr.pano.valid[0].any() and not dr.pano.valid[-1].any()  # pole rows never survive
-    assert np.mean(agree) >= 0.97 and np.mean(close) >= 0.97, (agree, close)
+    assert np.mean(agree) >= 0.995 and np.mean(close) >= 0.995, (agree, close)  # north_star's bar
+    assert min(agree) >= 0.99 and min(close) >= 0.99, (agree, close)
+    # ... and the CPU oracle's own run of the same chain is reproduced (measured: every map identical)
+    want = oracle_chain(z)
+    for kid, dr in res.depths.items():
+        od, ov = want[kid]
+        assert (dr.pano.valid == ov).mean() >= 0.995
+        both = dr.pano.valid & ov
+        assert (np.abs(dr.pano.depth - od)[both] <= 0.005 * od[both]).mean() >= 0.995
     assert abs(rep["fused_points"] - int(z["fused_points"])) <= 0.05 * int(z["fused_points"])
     assert abs(rep["completeness"]["mean"] - float(z["comp_mean"])) <= 0.003
     assert len(rep["completeness"]["per_keyframe"]) == 20 and rep["resolution"] == [64, 32]

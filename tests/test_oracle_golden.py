@@ -162,8 +162,8 @@ def test_depth_stage_chain(oracle):
         agree.append(float((valid == z["stage_valid"][j]).mean()))
         both = valid & z["stage_valid"][j]
         rel = np.abs(depth - z["stage_depth"][j])[both] / z["stage_depth"][j][both]
-        assert (rel <= 0.005).mean() >= 0.99, (k, (rel <= 0.005).mean())
-    assert min(agree) >= 0.99, agree
+        assert (rel <= 0.005).mean() >= 0.995, (k, (rel <= 0.005).mean())  # north_star's bar, on every map
+    assert min(agree) >= 0.995, agree
 
 
 def test_philox_known_answers(oracle):
