@@ -220,8 +220,18 @@ int d360_fuse_oldest(const float *depth, const uint8_t *valid, const double *rot
                      uint32_t *block_counts, double *points, uint8_t *colors,
                      int64_t *n_points_host, int height, int width, void *stream);
 
-/* replaces synth.render_scene for box/corridor scenes (SY:66-84, SY:101-169): analytic
- * ray cast + 4-octave splitmix value noise, f64; image (H,W,3) u8, depth (H,W) f32. */
+/* replaces synth.render_scene (SY:154-169) with SyntheticScene.cast (SY:66-84) and .shade (SY:86-98):
+ * analytic ray cast of a closed scene seen from inside - kind 0: axis-aligned box / corridor of full extents
+ * size_xyz, kind 1: sphere shell of radius size_xyz[0] / 2 with oo_minus_r2 = o @ o - radius^2 evaluated by
+ * the caller - and its texture: multi-octave splitmix value noise (SY:101-151), or with checker != 0 the
+ * 40 / 215 checkerboard of SY:88-92 with noise_scale-sized cells.  f64 throughout; image (H,W,3) u8,
+ * depth (H,W) f32.  Bit-identical to the reference's images, rotations included (see the kernel's note on
+ * the two BLAS statements). */
+int d360_render_scene(int kind, int checker, const double *size_xyz, double oo_minus_r2,
+                      int texture_seed, double noise_scale, int octaves, const double *rot,
+                      const double *trans, const double *rays64, uint8_t *image, float *depth,
+                      int height, int width, void *stream);
+/* the same for kind 0 without checker (kept for callers of the first release) */
 int d360_render_box_scene(const double *size_xyz, int texture_seed, double noise_scale,
                           int octaves, const double *rot, const double *trans,
                           const double *rays64, uint8_t *image, float *depth, int height,

@@ -292,7 +292,35 @@ def offline_case():
           rep["completeness"]["mean"], ids, decisions[:4])
 
 
+def render_case():
+    """synth.render_scene (SY:154-169) for every scene kind, with rotated poses and the checker texture."""
+    cam = EquirectCamera(64, 32)
+    cases = [("sphere", False, RigidPose(np.eye(3), np.array([0.31, -0.27, 0.45]))),
+             ("sphere", False, RigidPose(rot(1, 33.0) @ rot(0, -12.0), np.array([-0.5, 0.2, 0.1]))),
+             ("box", True, RigidPose(rot(2, 8.0) @ rot(1, -21.0), np.array([0.4, -0.3, 0.9]))),
+             ("corridor", False, RigidPose(rot(0, 5.0) @ rot(1, 170.0), np.array([0.7, 0.4, -6.5]))),
+             ("box", False, RigidPose(rot(1, 91.0) @ rot(2, 45.0) @ rot(0, -30.0), np.array([-1.1, 0.9, 1.7])))]
+    out = {"kinds": np.array([c[0] for c in cases]), "checker": np.array([c[1] for c in cases]),
+           "rotations": np.stack([c[2].rotation for c in cases]), "translations": np.stack([c[2].translation for c in cases])}
+    imgs, depths = [], []
+    for kind, checker, pose in cases:
+        image, pano = render_scene(default_scene(kind, checker=checker), cam, pose)
+        imgs.append(image)
+        depths.append(pano.depth)
+    # a larger frame too: the BLAS kernels behind rays @ R.T may differ with the matrix size
+    big = EquirectCamera(512, 256)
+    image, pano = render_scene(default_scene("sphere"), big, cases[1][2])
+    from densify360.synth import straight_line_trajectory
+    traj = straight_line_trajectory(default_scene("corridor"), 9)
+    np.savez_compressed(OUT / "render_64x32.npz", images=np.stack(imgs), depths=np.stack(depths), big_image=image,
+                        big_depth=pano.depth, traj=np.stack([q.translation for q in traj]), **out)
+    print("render ok", [int(i.mean()) for i in imgs])
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["render"]:
+        render_case()
+        sys.exit(0)
     if sys.argv[1:] == ["io"]:
         io_metrics_case()
         sys.exit(0)
@@ -310,3 +338,4 @@ if __name__ == "__main__":
     misc_case()
     io_metrics_case()
     offline_case()
+    render_case()

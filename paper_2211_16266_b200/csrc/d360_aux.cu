@@ -535,34 +535,58 @@ struct SceneDev {
     double half[3];
     int texture_seed, octaves;
     double noise_scale;
+    int kind;             // 0: axis-aligned box / corridor (SY:76-84), 1: sphere shell (SY:70-74)
+    int checker;          // SY:88-92
+    double oo_minus_r2;   // sphere: o @ o - radius^2, evaluated by the caller with numpy like the reference
 };
 
-__global__ void k_render_box(const __grid_constant__ SceneDev sc, const __grid_constant__ Rigid pose,
-                             const double* __restrict__ rays64, uint8_t* __restrict__ image,
-                             float* __restrict__ depth, size_t n) {
+// render_scene, SY:154-169, statement by statement in f64.  Two of the reference's statements are BLAS
+// calls whose rounding numpy does not define; they are restated the way the reference's numpy evaluates
+// them on the build host (OpenBLAS FMA kernels; checked with exact rational arithmetic, all elements):
+//   camera_rays(camera) @ pose.rotation.T   (dgemm, k = 3)  ->  fma(a2, b2, fma(a1, b1, a0 * b0))
+//   d @ o                                   (dgemv, n = 3)  ->  fma(a2, b2, fma(a0, b0, a1 * b1))
+// With those the images are bit-identical to the reference's under any rotation and for the sphere scene
+// (goldens render_64x32.npz); on a host whose BLAS rounds differently the reference itself changes by the
+// same last bit.
+__global__ void k_render_scene(const __grid_constant__ SceneDev sc, const __grid_constant__ Rigid pose,
+                               const double* __restrict__ rays64, uint8_t* __restrict__ image,
+                               float* __restrict__ depth, size_t n) {
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double rx = rays64[3 * i], ry = rays64[3 * i + 1], rz = rays64[3 * i + 2];
     const double* r = pose.r;
     double d[3];
-    d[0] = dot3_f64(rx, ry, rz, r[0], r[1], r[2]);
-    d[1] = dot3_f64(rx, ry, rz, r[3], r[4], r[5]);
-    d[2] = dot3_f64(rx, ry, rz, r[6], r[7], r[8]);
-    double t = INFINITY;
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        const double bound = d[a] > 0 ? sc.half[a] : -sc.half[a];
-        const double ta = d[a] != 0.0 ? __dsub_rn(bound, pose.t[a]) / d[a] : INFINITY;
-        t = fmin(t, ta > 0 ? ta : INFINITY);
+    for (int a = 0; a < 3; ++a) d[a] = fma(rz, r[3 * a + 2], fma(ry, r[3 * a + 1], __dmul_rn(rx, r[3 * a])));
+    double t;
+    if (sc.kind == 1) {
+        const double od = fma(d[2], pose.t[2], fma(d[0], pose.t[0], __dmul_rn(d[1], pose.t[1])));
+        const double disc = __dsub_rn(__dmul_rn(od, od), sc.oo_minus_r2);
+        t = __dadd_rn(-od, sqrt(fmax(disc, 0.0)));
+    } else {
+        t = INFINITY;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const double bound = d[a] > 0 ? sc.half[a] : -sc.half[a];
+            const double ta = d[a] != 0.0 ? __dsub_rn(bound, pose.t[a]) / d[a] : INFINITY;
+            t = fmin(t, ta > 0 ? ta : INFINITY);
+        }
     }
     const double px = __dadd_rn(pose.t[0], __dmul_rn(t, d[0]));
     const double py = __dadd_rn(pose.t[1], __dmul_rn(t, d[1]));
     const double pz = __dadd_rn(pose.t[2], __dmul_rn(t, d[2]));
+    if (sc.checker) {
+        const long long cells = (long long)floor(px / sc.noise_scale) + (long long)floor(py / sc.noise_scale) +
+                                (long long)floor(pz / sc.noise_scale);
+        const uint8_t v = (cells & 1) == 0 ? 40 : 215;
+        image[3 * i] = image[3 * i + 1] = image[3 * i + 2] = v;
+    } else {
 #pragma unroll 1
-    for (int c = 0; c < 3; ++c) {
-        const double v = value_noise(px, py, pz, sc.noise_scale, sc.texture_seed + 101 * c, sc.octaves);
-        const double s = fmin(fmax(__dmul_rn(v, 255.0), 0.0), 255.0);
-        image[3 * i + c] = (uint8_t)s;  // astype(uint8) truncates
+        for (int c = 0; c < 3; ++c) {
+            const double v = value_noise(px, py, pz, sc.noise_scale, sc.texture_seed + 101 * c, sc.octaves);
+            const double s = fmin(fmax(__dmul_rn(v, 255.0), 0.0), 255.0);
+            image[3 * i + c] = (uint8_t)s;  // astype(uint8) truncates
+        }
     }
     depth[i] = (float)t;
 }
@@ -795,20 +819,39 @@ extern "C" int d360_fuse_oldest(const float* depth, const uint8_t* valid, const 
     return 0;
 }
 
-extern "C" int d360_render_box_scene(const double* size_xyz, int texture_seed, double noise_scale, int octaves,
-                                     const double* rot, const double* trans, const double* rays64,
-                                     uint8_t* image, float* depth, int height, int width, void* stream) {
+extern "C" int d360_render_scene(int kind, int checker, const double* size_xyz, double oo_minus_r2, int texture_seed,
+                                 double noise_scale, int octaves, const double* rot, const double* trans,
+                                 const double* rays64, uint8_t* image, float* depth, int height, int width,
+                                 void* stream) {
+    if (kind != 0 && kind != 1) {
+        set_error("scene kind %d is neither 0 (box / corridor) nor 1 (sphere)", kind);
+        return 1;
+    }
+    if (octaves < 1 || !(noise_scale > 0.0)) {
+        set_error("texture octaves must be >= 1 and noise_scale > 0, got %d, %g", octaves, noise_scale);
+        return 1;
+    }
     SceneDev sc;
     for (int a = 0; a < 3; ++a) sc.half[a] = size_xyz[a] / 2.0;
     sc.texture_seed = texture_seed;
     sc.octaves = octaves;
     sc.noise_scale = noise_scale;
+    sc.kind = kind;
+    sc.checker = checker != 0;
+    sc.oo_minus_r2 = oo_minus_r2;
     Rigid pose;
     fill_rigid(&pose, rot, trans);
     const size_t n = (size_t)height * width;
     {
-        TraceScope ts_("render_box", (cudaStream_t)stream);
-        k_render_box<<<blocks_for(n, 128), 128, 0, (cudaStream_t)stream>>>(sc, pose, rays64, image, depth, n);
+        TraceScope ts_("render_scene", (cudaStream_t)stream);
+        k_render_scene<<<blocks_for(n, 128), 128, 0, (cudaStream_t)stream>>>(sc, pose, rays64, image, depth, n);
     }
-    return check_launch("render_box_scene");
+    return check_launch("render_scene");
+}
+
+extern "C" int d360_render_box_scene(const double* size_xyz, int texture_seed, double noise_scale, int octaves,
+                                     const double* rot, const double* trans, const double* rays64,
+                                     uint8_t* image, float* depth, int height, int width, void* stream) {
+    return d360_render_scene(0, 0, size_xyz, 0.0, texture_seed, noise_scale, octaves, rot, trans, rays64, image, depth,
+                             height, width, stream);
 }

@@ -1,10 +1,11 @@
-"""Synthetic box / corridor scenes rendered on the GPU (benchmark and test input generator).
+"""Synthetic scenes rendered on the GPU (benchmark and test input generator).
 
 Re-implements the analytic scenes of the reference's ``densify360.synth`` (SY = synth.py
-there): closed axis-aligned box viewed from inside (SY:66-84) textured with 4-octave
-splitmix-hash value noise (SY:101-151).  The kernel follows the float64 numpy code operation
-by operation, so for identity rotations the image is bit-identical to ``render_scene``
-(SY:154-169); the reference's CPU render takes ~11 s per 1920x960 frame.
+there): closed axis-aligned box room, long-box corridor and sphere shell viewed from inside
+(SY:66-84), textured with 4-octave splitmix-hash value noise (SY:101-151) or the deliberately
+ambiguous checker (SY:88-92).  The kernel follows the float64 numpy code operation by operation
+(the two BLAS statements as the reference's numpy rounds them), so the images are bit-identical to
+``render_scene`` (SY:154-169) for any pose; the reference's CPU render takes ~11 s per 1920x960 frame.
 """
 from __future__ import annotations
 
@@ -19,18 +20,21 @@ from .errors import ConfigError
 from .geometry import EquirectCamera, GeometryError, RigidPose
 from .keyframes import Keyframe, StereoGroup
 
-SCENE_KINDS = ("box", "corridor")
+SCENE_KINDS = ("box", "corridor", "sphere")
 
 
 @dataclass(frozen=True)
 class SyntheticScene:
-    """Axis-aligned box room: full extents in metres, value-noise texture parameters."""
+    """Closed analytic scene (SY:27-64): full box extents in metres for box / corridor, ``(diameter,) * 3``
+    for the sphere shell; value-noise texture parameters, or the checker of ``noise_scale``-sized cells."""
 
     kind: str = "box"
     size: tuple = (4.0, 3.0, 5.0)
     texture_seed: int = 7
     noise_scale: float = 0.6
     octaves: int = 4
+    checker: bool = False
+    trajectory: tuple = ()
 
     def __post_init__(self) -> None:
         if self.kind not in SCENE_KINDS:
@@ -39,19 +43,50 @@ class SyntheticScene:
             raise ConfigError(f"scene size must be positive, got {self.size}")
         if self.octaves < 1:
             raise ConfigError(f"texture octaves must be >= 1, got {self.octaves}")
+        for pose in self.trajectory:
+            if not self.contains(pose.translation):
+                raise GeometryError(f"trajectory pose at {pose.translation} lies outside the scene")
+
+    @property
+    def radius(self) -> float:
+        return self.size[0] / 2.0
 
     def contains(self, point, margin: float = 0.05) -> bool:
+        pt = np.asarray(point, dtype=np.float64)
+        if self.kind == "sphere":
+            return float(np.linalg.norm(pt)) < self.radius - margin
         half = np.asarray(self.size, dtype=np.float64) / 2.0
-        return bool(np.all(np.abs(np.asarray(point, dtype=np.float64)) < half - margin))
+        return bool(np.all(np.abs(pt) < half - margin))
 
 
-def default_scene(kind: str) -> SyntheticScene:
+def straight_line_trajectory(scene: SyntheticScene, keyframes: int, span_fraction: float = 0.7) -> tuple:
+    """In-and-out flight along the scene's long axis with identity orientation (SY:172-200): a triangle
+    wave whose fold sits half a step past the apex, so the return leg interleaves the outbound grid."""
+    if keyframes < 1:
+        raise ConfigError(f"keyframes must be >= 1, got {keyframes}")
+    axis = np.zeros(3)
+    if scene.kind == "sphere":
+        axis[2] = 1.0
+        reach = scene.radius * span_fraction / 2.0
+    else:
+        extents = np.asarray(scene.size)
+        axis[int(np.argmax(extents))] = 1.0
+        reach = float(extents.max()) * span_fraction / 2.0
+    h = 4.0 / keyframes
+    raw = -1.0 + h * np.arange(keyframes)
+    s = np.where(raw > 1.0 + h / 4.0, 2.0 + h / 2.0 - raw, raw)
+    return tuple(RigidPose(rotation=np.eye(3), translation=axis * (si * reach)) for si in s)
+
+
+def default_scene(kind: str, keyframes: int = 0, checker: bool = False) -> SyntheticScene:
     """Presets of SY:203-224."""
-    if kind == "box":
-        return SyntheticScene("box", (4.0, 3.0, 5.0))
-    if kind == "corridor":
-        return SyntheticScene("corridor", (4.0, 3.0, 20.0))
-    raise ConfigError(f"scene kind must be one of {SCENE_KINDS}, got {kind!r}")
+    sizes = {"box": (4.0, 3.0, 5.0), "corridor": (4.0, 3.0, 20.0), "sphere": (4.0, 4.0, 4.0)}
+    if kind not in sizes:
+        raise ConfigError(f"scene kind must be one of {SCENE_KINDS}, got {kind!r}")
+    scene = SyntheticScene(kind, sizes[kind], checker=checker)
+    if keyframes:
+        scene = SyntheticScene(kind, sizes[kind], checker=checker, trajectory=straight_line_trajectory(scene, keyframes))
+    return scene
 
 
 def render_scene_device(scene: SyntheticScene, camera: EquirectCamera, pose: RigidPose, device=None):
@@ -65,12 +100,15 @@ def render_scene_device(scene: SyntheticScene, camera: EquirectCamera, pose: Rig
     size = np.ascontiguousarray(scene.size, dtype=np.float64)
     rot = np.ascontiguousarray(pose.rotation.reshape(9), dtype=np.float64)
     tr = np.ascontiguousarray(pose.translation, dtype=np.float64)
+    o = np.asarray(pose.translation, dtype=np.float64)
+    oo_minus_r2 = float(o @ o - scene.radius**2)  # SY:73, evaluated by numpy as the reference does
     with torch.cuda.device(dev):
         image = torch.empty((h, w, 3), dtype=torch.uint8, device=dev)
         depth = torch.empty((h, w), dtype=torch.float32, device=dev)
-        _lib.check(lib.d360_render_box_scene(size.ctypes.data, int(scene.texture_seed), float(scene.noise_scale),
-                                             int(scene.octaves), rot.ctypes.data, tr.ctypes.data, _ptr(cam.rays64),
-                                             _ptr(image), _ptr(depth), h, w, _stream()), "render_box_scene")
+        _lib.check(lib.d360_render_scene(1 if scene.kind == "sphere" else 0, int(bool(scene.checker)), size.ctypes.data,
+                                         oo_minus_r2, int(scene.texture_seed), float(scene.noise_scale),
+                                         int(scene.octaves), rot.ctypes.data, tr.ctypes.data, _ptr(cam.rays64),
+                                         _ptr(image), _ptr(depth), h, w, _stream()), "render_scene")
     return image, depth
 
 

@@ -442,10 +442,26 @@ def test_renderer_matches_reference_images(pkg):
         if k == 1:
             assert np.array_equal(pano.depth, z["gt_depth"])
     z = load_golden("hot_64x32_rot")
-    for k in range(3):
+    for k in range(3):  # rotated poses: bit-identical too (the kernel rounds rays @ R.T as the reference's numpy does)
         img, _ = synth.render_scene(scene, cam, p.RigidPose(z["rotations"][k], z["translations"][k]))
-        diff = np.abs(img.astype(int) - z["images"][k].astype(int))
-        assert diff.max() <= 1 and (diff > 0).mean() < 1e-3
+        assert np.array_equal(img, z["images"][k])
+    # every scene kind of SY:24 (sphere shell, checker texture, corridor), rotated poses, SY:66-98
+    z = load_golden("render_64x32")
+    for k, (kind, checker) in enumerate(zip(z["kinds"], z["checker"])):
+        sc = synth.default_scene(str(kind), checker=bool(checker))
+        pose = p.RigidPose(z["rotations"][k], z["translations"][k])
+        img, pano = synth.render_scene(sc, cam, pose)
+        assert np.array_equal(img, z["images"][k]), (k, kind)
+        assert np.array_equal(pano.depth, z["depths"][k]), (k, kind)
+    img, pano = synth.render_scene(synth.default_scene("sphere"), p.EquirectCamera(512, 256),
+                                   p.RigidPose(z["rotations"][1], z["translations"][1]))
+    assert np.array_equal(img, z["big_image"]) and np.array_equal(pano.depth, z["big_depth"])
+    traj = synth.straight_line_trajectory(synth.default_scene("corridor"), 9)
+    assert np.array_equal(np.stack([q.translation for q in traj]), z["traj"])
+    assert len(synth.default_scene("corridor", keyframes=9).trajectory) == 9
+    from paper_2211_16266_b200.geometry import GeometryError
+    with pytest.raises(GeometryError):
+        synth.render_scene(synth.default_scene("sphere"), cam, p.RigidPose(np.eye(3), np.array([0.0, 1.99, 0.0])))
 
 
 def test_full_size_properties(pkg):
