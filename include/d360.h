@@ -237,6 +237,18 @@ int d360_render_box_scene(const double *size_xyz, int texture_seed, double noise
                           const double *rays64, uint8_t *image, float *depth, int height,
                           int width, void *stream);
 
+/* replaces dataset.resample_keyframe (dataset.py:146-157) = Pillow Image.resize(size, LANCZOS) on an 8-bit
+ * (H,W) or (H,W,3) image (Pillow 12.2.0, src/libImaging/Resample.c: horizontal pass into a uint8 intermediate,
+ * then vertical pass; 22-bit fixed-point coefficients).  bounds_* (n_out, 2) = (first source index, tap count),
+ * kk_* (n_out, ksize_*) = integer coefficients, both on the device, computed by the caller as Pillow's
+ * precompute_coeffs + normalize_coeffs_8bpc do (paper_2211_16266_b200/ingest.py).  bounds_y must already be
+ * relative to row0; tmp holds (rows, dst_w, channels) bytes for source rows [row0, row0 + rows).  When only one
+ * axis changes Pillow skips the other pass; the caller then passes identity windows (one tap of 1 << 22). */
+int d360_resample_u8(const uint8_t *src, int src_h, int src_w, int channels, uint8_t *tmp, uint8_t *dst,
+                     int dst_h, int dst_w, const int32_t *bounds_x, const int32_t *kk_x, int ksize_x,
+                     const int32_t *bounds_y, const int32_t *kk_y, int ksize_y, int row0, int rows,
+                     void *stream);
+
 /* FP32-FMA peak microbenchmark used as the roofline denominator for the cost kernels
  * (MEASURED_PEAKS.json carries no FP32 figure).  Returns achieved TFLOP/s (FMA = 2),
  * fp64 != 0 measures the DFMA pipe instead.  Synchronous. */

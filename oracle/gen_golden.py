@@ -317,7 +317,26 @@ def render_case():
     print("render ok", [int(i.mean()) for i in imgs])
 
 
+def resample_case():
+    """dataset.resample_keyframe (dataset.py:146-157, Pillow LANCZOS): down, up, one axis only, gray."""
+    from densify360.dataset import resample_keyframe
+    cam = EquirectCamera(128, 64)
+    image, _ = render_scene(default_scene("box"), cam, RigidPose(np.eye(3), np.zeros(3)))
+    rng = np.random.default_rng(3)
+    noise = rng.integers(0, 256, (50, 100, 3), dtype=np.uint8)
+    out = {"src_box": image, "src_noise": noise}
+    for name, src, (w, h) in (("box_down", image, (64, 32)), ("box_up", image, (192, 96)), ("noise_to_64", noise, (64, 32)),
+                              ("noise_up", noise, (256, 128))):
+        kf = Keyframe(id=0, image=src, pose=RigidPose(np.eye(3), np.zeros(3)))
+        out[name] = resample_keyframe(kf, EquirectCamera(w, h)).image
+    np.savez_compressed(OUT / "resample_128x64.npz", **out)
+    print("resample ok", {k: v.shape for k, v in out.items()})
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["resample"]:
+        resample_case()
+        sys.exit(0)
     if sys.argv[1:] == ["render"]:
         render_case()
         sys.exit(0)
@@ -339,3 +358,4 @@ if __name__ == "__main__":
     io_metrics_case()
     offline_case()
     render_case()
+    resample_case()

@@ -32,6 +32,7 @@ _PIPELINE_NAMES = {
 }
 
 
+_INGEST_NAMES = {"resample_keyframe", "resample_image_device"}
 _OFFLINE_NAMES = {"ViewFilterConfig", "ViewFilterDecision", "view_filter_accept", "KeyframeBuffer", "PipelineResult",
                   "run_offline"}
 
@@ -50,4 +51,8 @@ def __getattr__(name):
         from . import offline
 
         return getattr(offline, name)
+    if name in _INGEST_NAMES:
+        from . import ingest
+
+        return getattr(ingest, name)
     raise AttributeError(f"module {__name__!r} has no attribute {name!r}")

@@ -68,6 +68,8 @@ _SIGNATURES = {
     "d360_fuse_blocks": (C.c_int, [C.c_int, C.c_int]),
     "d360_fuse_oldest": (C.c_int, [c_void] * 9 + [C.c_int, c_void, C.c_double, C.c_double] + [c_void] * 5 +
                          [C.c_int, C.c_int, c_void]),
+    "d360_resample_u8": (C.c_int, [c_void, C.c_int, C.c_int, C.c_int, c_void, c_void, C.c_int, C.c_int, c_void, c_void,
+                                   C.c_int, c_void, c_void, C.c_int, C.c_int, C.c_int, c_void]),
     "d360_render_scene": (C.c_int, [C.c_int, C.c_int, c_void, C.c_double, C.c_int, C.c_double, C.c_int, c_void, c_void,
                                     c_void, c_void, c_void, C.c_int, C.c_int, c_void]),
     "d360_render_box_scene": (C.c_int, [c_void, C.c_int, C.c_double, C.c_int, c_void, c_void, c_void, c_void,

@@ -195,6 +195,49 @@ __global__ void k_voxel_keys(const double* __restrict__ pts, size_t n, double vo
     keys[i] = key;
 }
 
+// ---------------------------------------------------------------------------------------
+// Image ingest: dataset.resample_keyframe (reference dataset.py:146-157) = Pillow's
+// Image.resize(..., LANCZOS) on 8-bit images.  Pillow is a third-party dependency absent from
+// /root/reference (pinned: Pillow 12.2.0 in this image); its published algorithm
+// (src/libImaging/Resample.c) is two separable passes - horizontal first, into a uint8
+// intermediate, then vertical - each a convolution with per-output-pixel windows [xmin, xmin + n)
+// and coefficients normalised and rounded to 22-bit fixed point; the accumulator starts at
+// 1 << 21 (round half up) and the result is (acc >> 22) clipped to [0, 255].  The windows and the
+// integer coefficients are computed on the host (ingest.py, Pillow's double arithmetic statement by
+// statement: a few hundred values), the byte work runs here: pure integer, so bit-exact.
+// HBM-bound: one read of the source, one write + read of the intermediate, one write.
+// ---------------------------------------------------------------------------------------
+constexpr int RESAMPLE_BITS = 22;
+
+__device__ __forceinline__ uint8_t clip8_fixed(int v) {
+    v >>= RESAMPLE_BITS;
+    return (uint8_t)(v < 0 ? 0 : (v > 255 ? 255 : v));
+}
+
+// One thread per output pixel, all channels.  horizontal: out (rows, out_w, C) from in rows [row0, row0 + rows)
+// of (in_h, in_w, C); vertical: out (out_h, w, C) from in (in_h, w, C).
+template <int C, bool VERTICAL>
+__global__ void k_resample(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, const int* __restrict__ bounds,
+                           const int* __restrict__ kk, int ksize, int in_w, int row0, int out_w, int out_h) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+    if (x >= out_w || y >= out_h) return;
+    const int o = VERTICAL ? y : x;
+    const int lo = __ldg(bounds + 2 * o), n = __ldg(bounds + 2 * o + 1);
+    const int* k = kk + (size_t)o * ksize;
+    int acc[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[c] = 1 << (RESAMPLE_BITS - 1);
+    for (int t = 0; t < n; ++t) {
+        const size_t src = VERTICAL ? ((size_t)(lo + t) * out_w + x) * C : ((size_t)(y + row0) * in_w + lo + t) * C;
+        const int w = __ldg(k + t);
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc[c] += (int)__ldg(in + src + c) * w;
+    }
+    const size_t dst = ((size_t)y * out_w + x) * C;
+#pragma unroll
+    for (int c = 0; c < C; ++c) out[dst + c] = clip8_fixed(acc[c]);
+}
+
 }  // namespace d360
 
 using namespace d360;
@@ -272,4 +315,35 @@ extern "C" int d360_voxel_keys(const double* points, int64_t n, double voxel, lo
         k_voxel_keys<<<io_blocks((size_t)n, 256), 256, 0, (cudaStream_t)stream>>>(points, (size_t)n, voxel, keys, overflow);
     }
     return check_launch("voxel_keys");
+}
+
+extern "C" int d360_resample_u8(const uint8_t* src, int src_h, int src_w, int channels, uint8_t* tmp, uint8_t* dst,
+                                int dst_h, int dst_w, const int32_t* bounds_x, const int32_t* kk_x, int ksize_x,
+                                const int32_t* bounds_y, const int32_t* kk_y, int ksize_y, int row0, int rows,
+                                void* stream) {
+    if (channels != 1 && channels != 3) {
+        set_error("resample: expected 1 or 3 channels, got %d", channels);
+        return 1;
+    }
+    if (src_h < 1 || src_w < 1 || dst_h < 1 || dst_w < 1 || ksize_x < 1 || ksize_y < 1 || row0 < 0 || rows < 1 ||
+        row0 + rows > src_h) {
+        set_error("resample: bad sizes (src %dx%d, dst %dx%d, rows [%d, %d))", src_w, src_h, dst_w, dst_h, row0,
+                  row0 + rows);
+        return 1;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    {   // horizontal pass over the source rows the vertical pass will read (Resample.c: ybox_first .. ybox_last)
+        dim3 grid((dst_w + 127) / 128, rows);
+        TraceScope ts_("resample_h", s);
+        if (channels == 3) k_resample<3, false><<<grid, 128, 0, s>>>(src, tmp, bounds_x, kk_x, ksize_x, src_w, row0, dst_w, rows);
+        else k_resample<1, false><<<grid, 128, 0, s>>>(src, tmp, bounds_x, kk_x, ksize_x, src_w, row0, dst_w, rows);
+    }
+    if (check_launch("resample/horizontal")) return 2;
+    {
+        dim3 grid((dst_w + 127) / 128, dst_h);
+        TraceScope ts_("resample_v", s);
+        if (channels == 3) k_resample<3, true><<<grid, 128, 0, s>>>(tmp, dst, bounds_y, kk_y, ksize_y, dst_w, 0, dst_w, dst_h);
+        else k_resample<1, true><<<grid, 128, 0, s>>>(tmp, dst, bounds_y, kk_y, ksize_y, dst_w, 0, dst_w, dst_h);
+    }
+    return check_launch("resample/vertical");
 }

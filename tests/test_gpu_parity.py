@@ -464,6 +464,34 @@ def test_renderer_matches_reference_images(pkg):
         synth.render_scene(synth.default_scene("sphere"), cam, p.RigidPose(np.eye(3), np.array([0.0, 1.99, 0.0])))
 
 
+def test_resample_keyframe_equals_pillow_lanczos(pkg):
+    """dataset.resample_keyframe (dataset.py:146-157): the device passes reproduce Pillow's LANCZOS resize bit
+    for bit - against the reference's own outputs (golden) and against Pillow on random images and on the
+    full-size ingest case (3840x1920 -> 1920x960)."""
+    p, _, _, _ = pkg
+    from PIL import Image
+    from paper_2211_16266_b200 import ingest
+    z = load_golden("resample_128x64")
+    pose = p.RigidPose(np.eye(3), np.zeros(3))
+    for name, src, (w, h) in (("box_down", "src_box", (64, 32)), ("box_up", "src_box", (192, 96)),
+                              ("noise_to_64", "src_noise", (64, 32)), ("noise_up", "src_noise", (256, 128))):
+        kf = p.Keyframe(id=5, image=z[src], pose=pose, sparse_points=np.ones((2, 3)))
+        out = ingest.resample_keyframe(kf, p.EquirectCamera(w, h))
+        assert np.array_equal(out.image, z[name]), name
+        assert out.id == 5 and out.pose is pose and np.array_equal(out.sparse_points, kf.sparse_points)
+    kf = p.Keyframe(id=1, image=z["src_box"], pose=pose)
+    assert ingest.resample_keyframe(kf, p.EquirectCamera(128, 64)) is kf  # same size: returned as is
+    rng = np.random.default_rng(0)
+    for sh, sw, w, h, gray in ((37, 74, 74, 20, True), (64, 128, 128, 32, False), (96, 192, 64, 96, False),
+                               (1920, 3840, 1920, 960, False), (480, 960, 1920, 960, False)):
+        img = rng.integers(0, 256, (sh, sw) if gray else (sh, sw, 3), dtype=np.uint8)
+        want = np.asarray(Image.fromarray(img).resize((w, h), Image.LANCZOS))
+        got = ingest.resample_image_device(img, w, h).cpu().numpy()
+        assert np.array_equal(got, want), (sh, sw, w, h)
+    with pytest.raises(ValueError):
+        ingest.resample_image_device(np.zeros((4, 8, 2), np.uint8), 4, 2)
+
+
 def test_full_size_properties(pkg):
     """BASELINE config C3 size (1920x960, V=4): size-independent properties."""
     p, engine, pipeline, synth = pkg

@@ -186,3 +186,32 @@ def test_thread_count_invariance(oracle):
     oracle.set_threads(0)
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+def test_lanczos_coefficients_reproduce_the_reference_resample():
+    """Host half of row f4's ingest (paper_2211_16266_b200/ingest.py): Pillow's precompute_coeffs /
+    normalize_coeffs_8bpc restated; a numpy emulation of the two integer passes with those windows equals the
+    reference's resample_keyframe outputs (golden), so the device kernels only have to do integer sums."""
+    from paper_2211_16266_b200 import ingest
+
+    def passes(img, w, h):
+        sh, sw = img.shape[:2]
+        bx, kx = ingest._identity_coefficients(sw) if sw == w else ingest.lanczos_coefficients(sw, w)
+        by, ky = ingest._identity_coefficients(sh) if sh == h else ingest.lanczos_coefficients(sh, h)
+        a = img.astype(np.int64).reshape(sh, sw, -1)
+        tmp = np.zeros((sh, w, a.shape[2]), np.int64)
+        for x in range(w):
+            lo, n = bx[x]
+            tmp[:, x] = np.clip(((a[:, lo:lo + n] * kx[x, :n, None].astype(np.int64)).sum(1) + (1 << 21)) >> 22, 0, 255)
+        out = np.zeros((h, w, a.shape[2]), np.int64)
+        for y in range(h):
+            lo, n = by[y]
+            out[y] = np.clip(((tmp[lo:lo + n] * ky[y, :n, None, None].astype(np.int64)).sum(0) + (1 << 21)) >> 22, 0, 255)
+        return out.astype(np.uint8).reshape((h, w) + img.shape[2:])
+
+    z = load_golden("resample_128x64")
+    for name, src, (w, h) in (("box_down", "src_box", (64, 32)), ("box_up", "src_box", (192, 96)),
+                              ("noise_to_64", "src_noise", (64, 32)), ("noise_up", "src_noise", (256, 128))):
+        assert np.array_equal(passes(z[src], w, h), z[name]), name
+    bounds, kk = ingest.lanczos_coefficients(128, 64)
+    assert kk.shape == (64, 13) and (kk.sum(1) - (1 << 22)).__abs__().max() <= 8  # weights sum to 1 in 22-bit fixed point
