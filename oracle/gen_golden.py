@@ -333,7 +333,24 @@ def resample_case():
     print("resample ok", {k: v.shape for k, v in out.items()})
 
 
+def dataset_case():
+    """synth.make_dataset (SY:252-330): manifest text and PNG bytes of a 5-keyframe corridor dataset."""
+    import hashlib
+    import tempfile
+    from densify360.synth import make_dataset
+    with tempfile.TemporaryDirectory() as tmp:
+        root = make_dataset(default_scene("corridor", keyframes=5), 5, 7, tmp, EquirectCamera(64, 32), seed=5)
+        manifest = (root / "dataset.json").read_bytes()
+        pngs = [np.frombuffer((root / f"kf{k:04d}.png").read_bytes(), np.uint8) for k in range(5)]
+    np.savez_compressed(OUT / "dataset_64x32.npz", manifest=np.frombuffer(manifest, np.uint8),
+                        **{f"png{k}": a for k, a in enumerate(pngs)})
+    print("dataset ok", hashlib.sha256(manifest).hexdigest()[:12], [len(a) for a in pngs])
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["dataset"]:
+        dataset_case()
+        sys.exit(0)
     if sys.argv[1:] == ["resample"]:
         resample_case()
         sys.exit(0)
@@ -359,3 +376,4 @@ if __name__ == "__main__":
     offline_case()
     render_case()
     resample_case()
+    dataset_case()

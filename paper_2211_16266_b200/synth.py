@@ -58,6 +58,25 @@ class SyntheticScene:
         half = np.asarray(self.size, dtype=np.float64) / 2.0
         return bool(np.all(np.abs(pt) < half - margin))
 
+    def cast(self, origin, directions) -> np.ndarray:
+        """Closest-hit distance for unit ``directions`` (..., 3) from ``origin`` (SY:66-84), on the host:
+        used for the few hundred sparse landmarks of ``make_sequence``; images go through the GPU kernel."""
+        o = np.asarray(origin, dtype=np.float64)
+        d = np.asarray(directions, dtype=np.float64)
+        if self.kind == "sphere":
+            od = d @ o
+            disc = od * od - (o @ o - self.radius**2)
+            return -od + np.sqrt(np.maximum(disc, 0.0))
+        half = np.asarray(self.size) / 2.0
+        t = np.full(d.shape[:-1], np.inf)
+        for axis in range(3):
+            da = d[..., axis]
+            with np.errstate(divide="ignore"):
+                bound = np.where(da > 0, half[axis], -half[axis])
+                ta = np.where(da != 0.0, (bound - o[axis]) / np.where(da == 0, 1, da), np.inf)
+            t = np.minimum(t, np.where(ta > 0, ta, np.inf))
+        return t
+
 
 def straight_line_trajectory(scene: SyntheticScene, keyframes: int, span_fraction: float = 0.7) -> tuple:
     """In-and-out flight along the scene's long axis with identity orientation (SY:172-200): a triangle
@@ -145,3 +164,78 @@ def make_group(scene: SyntheticScene, camera: EquirectCamera, center=(0.0, 0.0, 
         if k == 0:
             gt = pano.depth
     return StereoGroup(reference=frames[0], neighbors=tuple(frames[1:]), camera=camera), gt
+
+
+def scene_to_dict(scene: SyntheticScene) -> dict:
+    """The manifest's optional scene descriptor (SY:227-235)."""
+    return {"kind": scene.kind, "size": list(scene.size), "texture_seed": scene.texture_seed,
+            "noise_scale": scene.noise_scale, "octaves": scene.octaves, "checker": scene.checker}
+
+
+def make_sequence(scene: SyntheticScene, keyframes: int, sparse_density: int, camera: EquirectCamera = EquirectCamera(512, 256),
+                  seed: int = 11, device=None) -> list:
+    """The keyframes ``make_dataset`` (SY:252-330) writes, kept in memory: trajectory poses (the scene's, or
+    ``straight_line_trajectory``), GPU-rendered images, and the sliding window over one global landmark pool
+    (surface hits of random directions, cast from a camera near each landmark's window) that the view filter
+    keys on.  Same NumPy draws in the same order as the reference, so ids, poses and landmarks are identical."""
+    if keyframes < 3:
+        raise ConfigError(f"make_dataset needs keyframes >= 3, got {keyframes}")
+    if sparse_density < 1:
+        raise ConfigError(f"sparse_density must be >= 1, got {sparse_density}")
+    poses = scene.trajectory
+    if len(poses) != keyframes:
+        poses = straight_line_trajectory(scene, keyframes)
+    rng = np.random.default_rng(seed)
+    stride = max(1, sparse_density // 3)
+    pool_size = sparse_density + stride * (keyframes - 1)
+    dirs = rng.standard_normal((pool_size, 3))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    src = np.clip(np.arange(pool_size) // stride - 1, 0, keyframes - 1)
+    pool = np.empty((pool_size, 3))
+    for k in np.unique(src):
+        sel = src == k
+        origin = poses[k].translation
+        pool[sel] = origin + dirs[sel] * scene.cast(origin, dirs[sel])[:, None]
+    out = []
+    for k, pose in enumerate(poses):
+        image, _ = render_scene_device(scene, camera, pose, device)
+        out.append(Keyframe(id=k, image=image.cpu().numpy(), pose=pose,
+                            sparse_points=pool[k * stride: k * stride + sparse_density]))
+    return out
+
+
+def make_dataset(scene: SyntheticScene, keyframes: int, sparse_density: int, out_dir, camera: EquirectCamera = EquirectCamera(512, 256),
+                 seed: int = 11):
+    """Drop-in for synth.make_dataset (SY:252-330): the sequence of ``make_sequence`` written in the pipeline's
+    dataset directory format (``kfNNNN.png`` + ``dataset.json`` with the field names of dataset.py:40)."""
+    import json
+    from pathlib import Path
+
+    from PIL import Image
+
+    from .errors import DatasetError
+
+    frames = make_sequence(scene, keyframes, sparse_density, camera, seed)
+    out = Path(out_dir)
+    try:
+        out.mkdir(parents=True, exist_ok=True)
+    except OSError as exc:
+        raise DatasetError(f"cannot create dataset directory {out}: {exc}") from exc
+    entries = []
+    for kf in frames:
+        name = f"kf{kf.id:04d}.png"
+        try:
+            Image.fromarray(kf.image).save(out / name)
+        except OSError as exc:
+            raise DatasetError(f"cannot write image {out / name}: {exc}") from exc
+        entries.append({"id": kf.id, "image": name, "rotation": [float(v) for v in kf.pose.rotation.reshape(-1)],
+                        "translation": [float(v) for v in kf.pose.translation],
+                        "sparse_points": [[float(c) for c in pt] for pt in kf.sparse_points]})
+    manifest = {"camera": {"width": camera.width, "height": camera.height}, "keyframes": entries,
+                "synthetic": scene_to_dict(scene)}
+    try:
+        with open(out / "dataset.json", "w", encoding="utf-8") as fh:
+            json.dump(manifest, fh, indent=1)
+    except OSError as exc:
+        raise DatasetError(f"cannot write manifest {out / 'dataset.json'}: {exc}") from exc
+    return out

@@ -464,6 +464,22 @@ def test_renderer_matches_reference_images(pkg):
         synth.render_scene(synth.default_scene("sphere"), cam, p.RigidPose(np.eye(3), np.array([0.0, 1.99, 0.0])))
 
 
+def test_make_dataset_writes_the_reference_bytes(pkg, tmp_path):
+    """synth.make_dataset (SY:252-330): trajectory, landmark pool and GPU-rendered frames give the reference's
+    dataset.json text and PNG files byte for byte."""
+    p, _, _, synth = pkg
+    z = load_golden("dataset_64x32")
+    root = synth.make_dataset(synth.default_scene("corridor", keyframes=5), 5, 7, tmp_path, p.EquirectCamera(64, 32), seed=5)
+    assert (root / "dataset.json").read_bytes() == z["manifest"].tobytes()
+    for k in range(5):
+        assert (root / f"kf{k:04d}.png").read_bytes() == z[f"png{k}"].tobytes(), k
+    frames = synth.make_sequence(synth.default_scene("corridor"), 5, 7, p.EquirectCamera(64, 32), seed=5)
+    assert [f.id for f in frames] == list(range(5)) and frames[0].sparse_points.shape == (7, 3)
+    from paper_2211_16266_b200.errors import ConfigError
+    with pytest.raises(ConfigError):
+        synth.make_sequence(synth.default_scene("box"), 2, 7)
+
+
 def test_resample_keyframe_equals_pillow_lanczos(pkg):
     """dataset.resample_keyframe (dataset.py:146-157): the device passes reproduce Pillow's LANCZOS resize bit
     for bit - against the reference's own outputs (golden) and against Pillow on random images and on the
