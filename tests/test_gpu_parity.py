@@ -464,6 +464,37 @@ def test_renderer_matches_reference_images(pkg):
         synth.render_scene(synth.default_scene("sphere"), cam, p.RigidPose(np.eye(3), np.array([0.0, 1.99, 0.0])))
 
 
+def test_c3_chain_hashes_are_pinned(pkg):
+    """The gate for kernel work: two keyframes of the benchmark's warp-initialised C3 chain (1920x960, V = 4,
+    6 iterations, Philox fill) must hash to the values of the round-1 tree (profiles/hash_chain_r2.txt: depth and
+    normal identical to commit bd06b2f for every keyframe; the cost map of the Philox-started keyframe 0 differs
+    from round 1 in one pole-row pixel by 6 ulp and is pinned to this round's value)."""
+    import hashlib
+    import sys
+    p, engine, pipeline, synth = pkg
+    sys.path.insert(0, str(ROOT))
+    import bench
+    w, h, v, hw, stride, iters = bench.WORKLOADS["c3"]
+    cam = p.EquirectCamera(w, h)
+    spec = engine.PatchSpec(hw, stride, 1.2)
+    scene = synth.default_scene("box")
+    poses = [p.RigidPose(np.eye(3), t) for t in bench.sequence_positions(0)]
+    nb_order = [-1, 1, -2, 2]
+    order = bench.walk(2)
+    need = sorted({i + o for i in order for o in [0] + nb_order})
+    kfs = {k: p.Keyframe(id=k, image=synth.render_scene_device(scene, cam, poses[k])[0].cpu().numpy(), pose=poses[k])
+           for k in need}
+    stage = pipeline.DepthStage(cam, spec, bench.DEPTH_RANGE, iters, 0, warp=True, precision="mixed", init_rng="philox")
+    got = []
+    for i in order:
+        g = p.StereoGroup(reference=kfs[i], neighbors=tuple(kfs[i + o] for o in nb_order), camera=cam)
+        stage.process_device(engine.PreparedGroup(g, spec, precision="mixed"))
+        pm = stage._prev[0]
+        got.append(tuple(hashlib.sha256(a.cpu().numpy().tobytes()).hexdigest()[:16] for a in (pm.depth, pm.normal, pm.cost)))
+    assert got == [("415f340eb557faa1", "92bae7b85f00aa5f", "bcdb123c8c0943e6"),
+                   ("e456f6be852f9546", "8511f4b170520da7", "829915606d50e964")], got
+
+
 def test_make_dataset_writes_the_reference_bytes(pkg, tmp_path):
     """synth.make_dataset (SY:252-330): trajectory, landmark pool and GPU-rendered frames give the reference's
     dataset.json text and PNG files byte for byte."""
