@@ -26,10 +26,12 @@ from collections import deque
 from dataclasses import dataclass
 
 import numpy as np
+import torch
 
 from .engine import PatchSpec
 from .errors import ConfigError, OrderingError
 from .geometry import EquirectCamera
+from .ingest import resample_keyframe
 from .keyframes import Keyframe, StereoGroup
 from .pipeline import (ConsistencyConfig, DepthResult, FusedCloud, FusionConfig, StreamingDensifier, neighbor_order)
 
@@ -146,6 +148,8 @@ class PipelineResult:
     depths: dict
     report: dict
     camera: EquirectCamera
+    device_batches: list = None  # the fused batches as they left the fusion stage, still in HBM (DeviceFusedCloud):
+    #                              outputs.write_ply and metrics.completeness take these without a PCIe round trip
 
 
 def run_offline(keyframes, camera: EquirectCamera, *, viewfilter: ViewFilterConfig | None = None,
@@ -166,15 +170,14 @@ def run_offline(keyframes, camera: EquirectCamera, *, viewfilter: ViewFilterConf
                                 median_window=median_window, median_rel_threshold=median_rel_threshold, top_k=top_k,
                                 precision=precision, init_rng=init_rng, device=device)
     clock = {"ingest": 0.0, "depth": 0.0, "fuse": 0.0}
-    poses, depth_seconds, batches, filtered = [], [], [], {}
+    poses, depth_seconds, batches, device_batches, filtered = [], [], [], [], {}
     queue_peaks = {"jobs": 0, "depths": 0}
 
     def accepted_keyframes():
         for keyframe in keyframes:
             t0 = time.perf_counter()
-            if keyframe.image.shape[:2] != camera.shape:
-                raise ConfigError(f"keyframe {keyframe.id} image {keyframe.image.shape[:2]} does not match camera "
-                                  f"{camera.shape} (resampling belongs to the dataset loader, which is out of scope)")
+            if keyframe.image.shape[:2] != camera.shape:  # brought to the working resolution (LANCZOS)
+                keyframe = resample_keyframe(keyframe, camera)
             poses.append(keyframe.pose)
             decision, _ = buffer.submit(keyframe)
             clock["ingest"] += time.perf_counter() - t0
@@ -188,6 +191,7 @@ def run_offline(keyframes, camera: EquirectCamera, *, viewfilter: ViewFilterConf
             filtered[out.id] = DepthResult(out.id, out.pano, out.pose, out.image, 0.0)
             if out.cloud is not None:
                 batches.append(out.cloud)
+                device_batches.append(out.cloud_device)
         dt = time.perf_counter() - t0
         if stream.jobs > jobs_before:  # one depth job ran (asynchronously; the time includes the D2H of its output)
             depth_seconds.append(dt)
@@ -229,10 +233,14 @@ def run_offline(keyframes, camera: EquirectCamera, *, viewfilter: ViewFilterConf
             consume(kf)
 
     t0 = time.perf_counter()
-    batches.extend(stream.finish())
+    tail = stream.finish_device()
+    device_batches.extend(tail)
+    batches.extend(b.to_host() for b in tail)
     clock["fuse"] += time.perf_counter() - t0
     cloud = FusedCloud.concat(batches)
-    comp = completeness(cloud.points, poses, device=stream.device) if poses else {
+    nonempty = [b.points for b in device_batches if len(b)]
+    all_points = torch.cat(nonempty) if nonempty else cloud.points  # the cloud is still in HBM: no re-upload
+    comp = completeness(all_points, poses, device=stream.device) if poses else {
         "per_keyframe": [], "mean": 0.0, "point_count": 0, "resolution": [720, 360]}
     report = {
         "keyframes_total": buffer.submitted,
@@ -247,4 +255,4 @@ def run_offline(keyframes, camera: EquirectCamera, *, viewfilter: ViewFilterConf
         "completeness": comp,
         "resolution": [camera.width, camera.height],
     }
-    return PipelineResult(cloud=cloud, depths=filtered, report=report, camera=camera)
+    return PipelineResult(cloud=cloud, depths=filtered, report=report, camera=camera, device_batches=device_batches)

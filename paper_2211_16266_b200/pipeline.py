@@ -344,6 +344,7 @@ class StreamOutput:
     pose: RigidPose
     cloud: FusedCloud | None = None
     image: np.ndarray | None = None  # the reference keyframe's host image (as given to push)
+    cloud_device: "DeviceFusedCloud | None" = None  # the same batch still in HBM (writers and metrics read it there)
 
 
 class StreamingDensifier:
@@ -492,6 +493,7 @@ class StreamingDensifier:
             if self._fusion is not None:
                 batch = self._fusion.push_device(DeviceDepthResult(target.id, pano, target.pose, target.image))
                 out.cloud = None if batch is None else batch.to_host()
+                out.cloud_device = batch
             return [out]
         with torch.cuda.device(self.device):
             done, hd, hv = self._download_async(pano)
@@ -499,12 +501,17 @@ class StreamingDensifier:
         if self._fusion is not None:
             batch = self._fusion.push_device(DeviceDepthResult(target.id, pano, target.pose, target.image))
             out.cloud = None if batch is None else batch.to_host()
+            out.cloud_device = batch
         self._pending.append((done, out, hd, hv))
         return self._collect(1)
 
     def finish(self) -> list:
         """Flush the fusion FIFO; frames still inside the consistency window are
         dropped, as in the reference."""
+        return [b.to_host() for b in self.finish_device()]
+
+    def finish_device(self) -> list:
+        """``finish`` with the batches left in HBM (DeviceFusedCloud)."""
         if self._fusion is None:
             return []
-        return [b.to_host() for b in self._fusion.flush_device()]
+        return self._fusion.flush_device()

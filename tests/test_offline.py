@@ -134,6 +134,16 @@ def test_run_offline_matches_reference_run():
     assert abs(rep["completeness"]["mean"] - float(z["comp_mean"])) <= 0.003
     assert len(rep["completeness"]["per_keyframe"]) == 20 and rep["resolution"] == [64, 32]
     assert np.all(np.diff(res.cloud.source_ids) >= 0) and len(res.cloud) == rep["fused_points"]
+    # the fused batches are also handed back where they were produced, in HBM: same points, written without a
+    # host round trip
+    assert sum(len(b) for b in res.device_batches) == len(res.cloud)
+    assert np.array_equal(np.concatenate([b.points.cpu().numpy() for b in res.device_batches if len(b)]), res.cloud.points)
+    # a keyframe at another resolution is brought to the working camera (LANCZOS) instead of rejected
+    from paper_2211_16266_b200 import ingest
+    big = [p.Keyframe(id=k.id, image=ingest.resample_image_device(k.image, 128, 64).cpu().numpy(), pose=k.pose,
+                      sparse_points=k.sparse_points) for k in kfs[:8]]
+    small = offline.run_offline(big, cam, **kw)
+    assert small.report["keyframes_total"] == 8 and all(d.pano.depth.shape == (32, 64) for d in small.depths.values())
     # fused points back-project onto the stored filtered depth maps (tests/test_pipeline.py:311-323)
     for src in np.unique(res.cloud.source_ids):
         dr = res.depths[int(src)]
