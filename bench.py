@@ -301,9 +301,23 @@ def run_product(args) -> dict | None:
             dist.barrier()
             torch.cuda.synchronize()
 
-    for i in order[:args.warmup]:
+    # warm-up; its first keyframe has no previous map to warp from, so it is the stream's cold start (every
+    # hypothesis drawn by Philox): timed on its own and reported beside the steady state
+    cold = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    if args.warmup:  # one keyframe through a scratch stage first: one-time set-up (ray tables, kernel attributes, allocator)
+        scratch_stage, stage = stage, make_stage()
+        g0 = group_of(order[0])
+        scratch_stage.process_device(engine.PreparedGroup(g0, spec, precision=args.precision, device=dev))
+        del scratch_stage, g0
+    for n_w, i in enumerate(order[:args.warmup]):
+        if n_w == 0:
+            torch.cuda.synchronize()
+            cold[0].record()
         step_device(i)
+        if n_w == 0:
+            cold[1].record()
     barrier()
+    cold_ms = cold[0].elapsed_time(cold[1]) if args.warmup else None
     stage.workspace.n_evals.zero_()
     _lib.trace_enable(True)
     launches0 = _lib.launch_count()
@@ -432,6 +446,12 @@ def run_product(args) -> dict | None:
                     "h2d_bytes_per_step": bytes_in // args.steps, "d2h_bytes_per_step": bytes_out // args.steps,
                     "ms_per_step": round(e2e_ms / args.steps, 3)},
             "gpu_launches": int(launches),
+            "generic_fallbacks": int(_lib.generic_fallbacks()),
+            "cold_start": {"ms_first_keyframe": None if cold_ms is None else round(cold_ms, 3),
+                           "maps_per_s": None if not cold_ms else round(1e3 / cold_ms, 3),
+                           "what": "first keyframe of the stream: no previous map to warp from, every hypothesis drawn "
+                                   "by Philox; `value` is the "
+                                   "warp-initialised steady state the reference's stream also runs in (P:213-232)"},
             "roofline": roofline,
             "kernels": kinds,
             "evals_per_step": {k: v // args.steps for k, v in evals.items()},
