@@ -299,16 +299,25 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
 
     // ---- phase 3
     if (live) {
+        // Remembered costs (computed by an earlier pass for the same (pixel, hypothesis)) are fetched first, as up to
+        // eight independent loads: taken one by one inside the arg-min loop they were eight dependent memory
+        // latencies per pixel, which is most of what a launch costs once the propagation has gone sparse.
+        const unsigned from_memo = considered & ~mask;
+        double remembered_cost[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            remembered_cost[j] = (from_memo >> j & 1u) ? __ldcs(memo_cost + 8 * i + j) : 0.0;
         double bc = (double)cost_in[i];
         int bj = -1;
-        for (unsigned m = considered; m; m &= m - 1) {
-            const int j = __ffs(m) - 1;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (!(considered >> j & 1u)) continue;
             double c;
             if (mask >> j & 1u) {
                 c = q.costs[tid * 8 + j];
                 if (memo_cost != nullptr) __stcs(memo_cost + 8 * i + j, c);
             } else {
-                c = __ldcs(memo_cost + 8 * i + j);  // computed by an earlier pass for the same (pixel, hypothesis)
+                c = remembered_cost[j];
             }
             if (c < bc) {  // K:463
                 bc = c;
