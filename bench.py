@@ -227,7 +227,13 @@ def run_product(args) -> dict | None:
         else:
             dist.init_process_group(backend)
     _lib.load()
-    if world > 1:
+    if world == 1 and args.sequence:
+        # the N = 1 point of the C5 curve: the same sharded-sequence code on one rank (one-rank process group,
+        # so the exchange / gather calls are the ones N > 1 runs; no halo exists, the gather is local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 2000))
+        dist.init_process_group(backend, rank=0, world_size=1, **({"device_id": dev} if backend == "nccl" else {}))
+    if world > 1 or args.sequence:
         out = run_product_sharded(args, world, rank, dev, backend)
         dist.barrier()
         dist.destroy_process_group()
@@ -815,6 +821,9 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c3")
+    ap.add_argument("--sequence", action="store_true",
+                    help="N = 1 only: run the sharded-sequence path of N > 1 (BASELINE config C5: depth maps + consistency + "
+                         "fusion + cloud gather over one sequence of --steps results) on the single GPU")
     ap.add_argument("--precision", choices=("mixed", "exact"), default="mixed")
     ap.add_argument("--no-cpu-baseline", action="store_true", help="skip the cpu_baseline leg (N=1 only)")
     args = ap.parse_args()
