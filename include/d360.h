@@ -93,7 +93,8 @@ int d360_version(void);
 unsigned long long d360_launch_count(void);
 /* Launches that ran on the generic kernels (csrc/d360_patchmatch.cu, about 2x slower) although the
  * MIXED policy was requested, because the throughput kernels do not cover the group: irregular sample
- * pattern, no padded f64 planes (nb64 / pads), a padded plane of 2^23 texels or more, or a patch window
+ * pattern, no padded f64 planes (nb64 / pads), a padded plane of 2^23 texels or more together with a patch other
+ * than the default 5x5 stride-2 one (with the default patch such planes stay on the throughput kernels), or a patch window
  * above 200 KB of shared memory.  The first launch of each reason is also reported on stderr (silenced by
  * the environment variable D360_QUIET_FALLBACK).  The reference has no such split (one numba path). */
 unsigned long long d360_generic_fallbacks(void);

@@ -96,15 +96,19 @@ bool make_fast_group(const GroupDev& gd, FastGroup* out) {
     if (gd.nb_pad_x < 1 || gd.nb_pad_y < 1 || gd.nb64 == nullptr)  // needs padded f64 planes
         return no("the group carries no padded f64 {value, dx} neighbour planes (d360_group.nb64, pads >= 1)");
     const long long pitch = gd.W + 2 * gd.nb_pad_x, rows = gd.H + 2 * gd.nb_pad_y;
-    if (pitch * rows >= (1ll << 23))  // f32 index arithmetic must stay exact
-        return no("a padded neighbour plane has 2^23 texels or more (beyond 3840x1920)");
+    // up to 2^23 texels per plane the texel index is formed in f32 (exact); beyond that (3840x1920 is the last size
+    // below) row and column are combined in integer arithmetic, Cfg::BIG
+    const bool big = pitch * rows >= (1ll << 23);
+    if (pitch >= (1ll << 22) || rows >= (1ll << 22)) return no("a neighbour plane side of 2^22 texels or more");
     FastGroup& g = *out;
     g.W = gd.W; g.H = gd.H; g.ns = ns; g.stride = stride; g.reach = half * stride; g.top_k = gd.top_k;
     g.pitch = (int)pitch;
     g.plane = (size_t)(pitch * rows);
     g.max_idx = (unsigned)(pitch * rows - pitch - 2);
     g.pitch_f = (float)pitch;
-    g.idx_bias = 8388608.0f + (float)(gd.nb_pad_y * pitch + gd.nb_pad_x);
+    g.big = big ? 1 : 0;
+    g.idx_bias = big ? 8388608.0f + (float)gd.nb_pad_x : 8388608.0f + (float)(gd.nb_pad_y * pitch + gd.nb_pad_x);
+    g.big_const = (unsigned)(((long long)gd.nb_pad_y - (1ll << 22)) * pitch);
     g.rays = gd.rays; g.ref_gray = gd.ref_gray; g.nb64 = gd.nb64;
     for (int v = 0; v < gd.V; ++v) {
         for (int i = 0; i < 9; ++i) g.rel_r[v][i] = gd.rel_r[v][i];

@@ -68,14 +68,18 @@ struct FastGroup {
     double neg_par_eps, tiny, c0375;  // -PARALLEL_EPS, 1e-30 (K:246), 3/8: 64-bit literals live in the constant bank
     unsigned plane32;     // plane as a 32-bit element count
     float pitch_f;        // pitch as float
-    float idx_bias;       // 2^23 + pad_y * pitch + pad_x: float -> index by mantissa extraction
+    float idx_bias;       // 2^23 + pad_y * pitch + pad_x: float -> index by mantissa extraction (big planes: 2^23 + pad_x)
     float den_lim;        // largest f32 below -PARALLEL_EPS
+    int big;              // a plane holds 2^23 texels or more: row and column are combined in integer arithmetic
+    unsigned big_const;   // (pad_y - 2^22) * pitch, mod 2^32: the row bias of the 1.5 * 2^23 floor, see gather_bilinear
 };
 
-// V views, NS x NS samples at stride ST (NS = 0: taken from the FastGroup at run time).
-template <int V_, int NS_, int ST_>
+// V views, NS x NS samples at stride ST (NS = 0: taken from the FastGroup at run time).  BIG: padded planes of
+// 2^23 texels or more (beyond 3840x1920, e.g. the paper's 5760x2880 quality mode), see gather_bilinear.
+template <int V_, int NS_, int ST_, bool BIG_ = false>
 struct Cfg {
     static constexpr int VT = V_, V = V_;
+    static constexpr bool BIG = BIG_;
     static constexpr int NT = D360_NT;
     static constexpr int MINB = D360_MINB;
     static constexpr int TH_FULL = NT / TW;    // eval / refine: NT pixels per CTA
@@ -352,7 +356,7 @@ __device__ __forceinline__ void project_uv(const FastGroup& g, double c38, const
 // cost of low-texture patches, measured).  floor by the 1.5 * 2^23 magic add; the element index
 // is formed in f32 (exact below 2^23) and read out of the mantissa, so no F2I / I2F conversions
 // are issued; all offsets are 32-bit element indices from one base.
-template <int VT, int PERIOD = VT>
+template <int VT, int PERIOD = VT, bool BIG = false>
 __device__ __forceinline__ void gather_bilinear(const FastGroup& g, const double2* __restrict__ nb,
                                                 unsigned plane_stride, const float (&pu)[VT], const float (&pv)[VT],
                                                 double (&val)[VT]) {
@@ -360,18 +364,27 @@ __device__ __forceinline__ void gather_bilinear(const FastGroup& g, const double
     // an integer M in [2^23, 2^24) (ulp 1).  For u the constant is idx_bias = 2^23 + pad_y * pitch +
     // pad_x, so the biased floor is already the low part of the texel index.
     const float MAGIC = 12582912.0f;  // 1.5 * 2^23
-    float fl_u[VT], fl_v[VT], bu[VT];
+    float fl_u[VT], fl_v[VT], bu[VT], bv[VT];
 #pragma unroll
     D360_FORV {
         bu[v] = __fadd_rd(pu[v], g.idx_bias);
         fl_u[v] = __fadd_rn(bu[v], -g.idx_bias);
-        fl_v[v] = __fadd_rn(__fadd_rd(pv[v], MAGIC), -MAGIC);
+        bv[v] = __fadd_rd(pv[v], MAGIC);
+        fl_v[v] = __fadd_rn(bv[v], -MAGIC);
     }
     unsigned idx[VT];
 #pragma unroll
     D360_FORV {
-        const float off = fmaf(fl_v[v], g.pitch_f, bu[v]);  // exact: < 2^24
-        idx[v] = min((unsigned)__float_as_int(off) & 0x7fffffu, g.max_idx);
+        if constexpr (BIG) {
+            // 2^23 texels or more per plane: row * pitch + column no longer fits f32 arithmetic, so the two biased
+            // floors are read out of their mantissas separately (column + pad_x; row + 2^22) and combined by one IMAD
+            const unsigned iu = (unsigned)__float_as_int(bu[v]) & 0x7fffffu;
+            const unsigned iv = (unsigned)__float_as_int(bv[v]) & 0x7fffffu;
+            idx[v] = min(iv * (unsigned)g.pitch + iu + g.big_const, g.max_idx);
+        } else {
+            const float off = fmaf(fl_v[v], g.pitch_f, bu[v]);  // exact: < 2^24
+            idx[v] = min((unsigned)__float_as_int(off) & 0x7fffffu, g.max_idx);
+        }
     }
     double2 r0[VT], r1[VT];  // { value, value(x+1) - value }
 #pragma unroll
@@ -520,7 +533,7 @@ __device__ __forceinline__ void accumulate_views_multi(const FastGroup& g, const
             plane_depth(es[j], lam[j], rvf[j], par[j]);
         }
         project_uv<SPT * NV>(g, c38, tx, ty, tz, pu, pv);
-        gather_bilinear<SPT * NV, NV>(g, nb, g.plane32, pu, pv, val);
+        gather_bilinear<SPT * NV, NV, C::BIG>(g, nb, g.plane32, pu, pv, val);
 #pragma unroll
         for (int j = 0; j < SPT; ++j) {
 #pragma unroll
@@ -541,7 +554,7 @@ __device__ __forceinline__ void accumulate_views_multi(const FastGroup& g, const
             const double rv = (double)rvf[j];
             bad = bad || par[j];
             project_uv<NV>(g, c38, tx, ty, tz, pu, pv);
-            gather_bilinear<NV>(g, nb, g.plane32, pu, pv, val);
+            gather_bilinear<NV, NV, C::BIG>(g, nb, g.plane32, pu, pv, val);
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
                 s0[v] += val[v];
@@ -721,7 +734,9 @@ static int prepare(K kernel, size_t smem) {
 }
 
 #define D360_FAST_GEO(V, ...)                                                         \
-    if (g.ns == 5 && g.stride == 2) { using C = Cfg<V, 5, 2>; __VA_ARGS__; }          \
+    if (g.ns == 5 && g.stride == 2 && g.big) { using C = Cfg<V, 5, 2, true>; __VA_ARGS__; } \
+    else if (g.big) return fast_reject("planes of 2^23 texels or more are covered for the default 5x5 stride-2 patch only"); \
+    else if (g.ns == 5 && g.stride == 2) { using C = Cfg<V, 5, 2>; __VA_ARGS__; }     \
     else { using C = Cfg<V, 0, 0>; __VA_ARGS__; }
 
 #define D360_FAST_DISPATCH(V, ...)                                                    \

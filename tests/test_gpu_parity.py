@@ -495,6 +495,48 @@ def test_c3_chain_hashes_are_pinned(pkg):
                    ("e456f6be852f9546", "8511f4b170520da7", "829915606d50e964")], got
 
 
+def test_planes_beyond_2_23_texels_stay_on_the_throughput_kernels(pkg, oracle):
+    """4096x2048 (padded planes of 8.41 M texels > 2^23; the paper's quality mode is 5760x2880): the texel index no
+    longer fits f32 arithmetic, the kernels combine row and column in integer arithmetic (Cfg::BIG).  Costs vs the
+    oracle on every pixel, one red-black and one refinement pass vs the literal policy, and no generic fallback."""
+    p, engine, _, synth = pkg
+    from paper_2211_16266_b200 import _lib
+    cam = p.EquirectCamera(4096, 2048)
+    group, gt = synth.make_group(synth.default_scene("box"), cam, n_views=2)
+    spec = engine.PatchSpec()
+    before = _lib.generic_fallbacks()
+    prep = engine.prepare_group(group, spec, precision="mixed")
+    rng = np.random.default_rng(0)
+    rays = p.camera_rays(cam)
+    n = -rays + rng.normal(0, 0.15, rays.shape)
+    n = (n / np.linalg.norm(n, axis=-1, keepdims=True)).astype(np.float32)
+    d = (gt * (1 + rng.normal(0, 0.01, gt.shape))).astype(np.float32)
+    dr = (0.5, 16.0)
+    pm = engine.DevicePlaneMap.from_host(engine.PlaneMap(cam, d, n, np.full(cam.shape, np.inf, np.float32),
+                                                         np.ones(cam.shape, bool), dr))
+    engine.evaluate_costs_device(prep, pm)
+    got = pm.cost.cpu().numpy()
+    want = oracle.eval_costs(_oracle_group(oracle, group, 5, 2), d, n)
+    ok = cost_close(got, want)
+    assert ok.mean() >= 1 - 1e-5, (1 - ok.mean(), np.abs(got - want).max())
+    # one propagation and one refinement pass against the literal policy (generic kernels, IEEE arithmetic)
+    lit = engine.prepare_group(group, spec, precision="exact")
+    src_l = engine.DevicePlaneMap.from_host(engine.PlaneMap(cam, d, n, got.copy(), np.ones(cam.shape, bool), dr))
+    outs = []
+    for pr in (prep, lit):
+        src = src_l.clone()
+        dst = src.clone()
+        engine.red_black_pass_device(pr, 0, src, dst)
+        engine.refine_pass_device(pr, dst, engine.refinement_draw_tables(3, 1, 0.25 * 15.5, np.radians(60.0))[0], dr)
+        outs.append(dst)
+    same = (outs[0].depth == outs[1].depth) & (outs[0].normal == outs[1].normal).all(-1)
+    assert same.float().mean().item() >= 0.9995
+    a, b = outs[0].cost.cpu().numpy(), outs[1].cost.cpu().numpy()
+    sm = same.cpu().numpy()
+    assert cost_close(a[sm], b[sm]).mean() >= 1 - 1e-5
+    assert _lib.generic_fallbacks() == before  # the mixed policy never left the throughput kernels
+
+
 def test_make_dataset_writes_the_reference_bytes(pkg, tmp_path):
     """synth.make_dataset (SY:252-330): trajectory, landmark pool and GPU-rendered frames give the reference's
     dataset.json text and PNG files byte for byte."""
