@@ -6,7 +6,8 @@ import paper_2211_16266_b200 as p
 from paper_2211_16266_b200 import engine, synth, _lib
 
 CONFIGS = {"c1": (256, 128, 2, 5, 2, 3, "box"), "c2": (960, 480, 4, 3, 1, 6, "box"), "c3": (1920, 960, 4, 5, 2, 6, "box"),
-           "c4": (3840, 1920, 6, 5, 2, 6, "corridor"), "c4s1": (3840, 1920, 6, 5, 1, 1, "corridor")}
+           "c4": (3840, 1920, 6, 5, 2, 6, "corridor"), "c4s1": (3840, 1920, 6, 5, 1, 1, "corridor"),
+           "quality": (5760, 2880, 4, 5, 2, 6, "box")}  # the paper's quality-mode resolution: planes > 2^23 texels
 for name in sys.argv[1:] or list(CONFIGS):
     W, H, V, hw, st, it, kind = CONFIGS[name]
     cam = p.EquirectCamera(W, H)
