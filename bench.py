@@ -498,13 +498,14 @@ def run_product_sharded(args, world: int, rank: int, dev, backend: str) -> dict 
     refs = [(i + half_v, pose_of(i + half_v)) for i in range(n_results)]
     plan = sequence.plan_shards(n_results, world, ccfg.window, fcfg.buffer)[rank]
     mine = range(max(0, plan.depth.start), min(n_kf, plan.depth.stop + 2 * half_v)) if len(plan.depth) else range(0)
-    dev_imgs, host_imgs = {}, {}
+    dev_imgs, host_imgs, pinned_imgs = {}, {}, {}
     for j in mine:  # the keyframes this rank's groups read: resident on the device and in pinned host memory
         img, _ = synth.render_scene_device(scene, cam, pose_of(j), dev)
         dev_imgs[j] = img
         pinned = torch.empty(img.shape, dtype=torch.uint8).pin_memory()
         pinned.copy_(img)
         host_imgs[j] = pinned.numpy()
+        pinned_imgs[j] = pinned  # the same memory as a tensor: DeviceKeyframe copies it up asynchronously
     torch.cuda.synchronize()
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     comm_device = None if backend == "nccl" else "cpu"
@@ -587,7 +588,7 @@ def run_product_sharded(args, world: int, rank: int, dev, backend: str) -> dict 
     gc.disable()
     barrier()
     t0 = time.perf_counter()
-    cloud_h, _ = run(host_imgs, stats_h)  # frames from pinned host memory, cloud to host on rank 0
+    cloud_h, _ = run(pinned_imgs, stats_h)  # frames from pinned host memory, cloud to host on rank 0
     stats_h.pop("stage", None)
     barrier()
     e2e_s = time.perf_counter() - t0

@@ -65,6 +65,18 @@ def _up(a: np.ndarray, dtype, device) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(a, dtype=dtype)).to(device, non_blocking=False)
 
 
+def _image_on_device(image, device) -> torch.Tensor:
+    """uint8 image as a tensor on ``device``.  CUDA tensors pass through; a CPU tensor in pinned memory is copied
+    asynchronously on the current stream (the caller keeps it alive and unchanged until that copy has run - the
+    contract of every pinned staging buffer), so the host does not wait for the kernels already queued; numpy
+    arrays and pageable tensors take the blocking copy."""
+    if isinstance(image, torch.Tensor):
+        if image.device.type == "cuda":
+            return image
+        return image.contiguous().to(device, non_blocking=image.is_pinned())
+    return _up(np.asarray(image), np.uint8, device)
+
+
 class DeviceCamera:
     """Per-(camera, device) constants: trig tables and pixel rays in f32 and f64."""
 
@@ -243,7 +255,7 @@ def to_gray_device(image, device=None, out: torch.Tensor | None = None, pad=(0, 
     neighbour (layout of ``d360_group.nb64``)."""
     dev = _device(device)
     lib = _lib.load()
-    img = image if isinstance(image, torch.Tensor) else _up(np.asarray(image), np.uint8, dev)
+    img = _image_on_device(image, dev)
     if img.dtype != torch.uint8:
         raise ValueError(f"expected a uint8 image, got {img.dtype}")
     if img.ndim == 2:
@@ -286,7 +298,7 @@ class DeviceKeyframe:
         self.device = _device(device)
         h, w = camera.shape
         with torch.cuda.device(self.device):
-            img = image if isinstance(image, torch.Tensor) else _up(np.asarray(image), np.uint8, self.device)
+            img = _image_on_device(image, self.device)
             if tuple(img.shape[:2]) != (h, w):
                 raise ValueError(f"image {tuple(img.shape[:2])} does not match camera {(h, w)}")
             self.image = img
