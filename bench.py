@@ -549,16 +549,10 @@ def run_product_sharded(args, world: int, rank: int, dev, backend: str) -> dict 
         return sequence.densify_sequence(groups, stage_factory, ccfg, fcfg, rank=rank, world=world, refs=refs,
                                          comm_device=comm_device, stats=stats)
 
-    # warm-up: kernels, allocator, NCCL channels (a short sequence through the same path)
-    warm_stage = pipeline.DepthStage(cam, spec, DEPTH_RANGE, iters, SEED, warp=True, precision=args.precision,
-                                     init_rng="philox", device=dev)
-    if len(plan.depth):
-        for _ in range(args.warmup):
-            c = plan.depth.start + half_v
-            kfs = [p.Keyframe(id=c, image=host_imgs[c], pose=pose_of(c))] + \
-                  [p.Keyframe(id=c + o, image=host_imgs[c + o], pose=pose_of(c + o)) for o in nb_order]
-            warm_stage.process_device(p.StereoGroup(reference=kfs[0], neighbors=tuple(kfs[1:]), camera=cam))
-    del warm_stage
+    # warm-up: one untimed pass over the same sequence through the same path - kernels, the caching allocator (the pass
+    # keeps ~1 GB of depth results alive; a cold allocator answers with synchronising cudaMallocs), NCCL channels
+    if args.warmup:
+        run(dev_imgs, {})
     tok = torch.zeros(1, device=dev if backend == "nccl" else "cpu")
     dist.all_reduce(tok)
     barrier()
