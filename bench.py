@@ -14,6 +14,9 @@ paper_2211_16266_b200.sequence.densify_sequence: every rank computes its block o
 exchanges the consistency / fusion halos with its neighbours point to point over NCCL, fuses its
 centres, and the cloud is gathered to rank 0 - all inside the timed region.
 
+SM clock and throttle reasons are sampled every 0.1 s during the timed region (NVML, the library behind
+nvidia-smi, in-process; the command-line tool as fallback) and reported under `clocks`.
+
 Prints ONE JSON line (rank 0).  `value` = keyframes of all ranks / max-over-ranks device
 time with the uint8 frames already resident in HBM; `e2e` = the same through the host-array
 streaming API (numpy frames in pinned memory -> StreamingDensifier.push -> numpy depth + mask)
