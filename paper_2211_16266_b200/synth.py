@@ -59,42 +59,45 @@ class SyntheticScene:
         return bool(np.all(np.abs(pt) < half - margin))
 
     def cast(self, origin, directions) -> np.ndarray:
-        """Closest-hit distance for unit ``directions`` (..., 3) from ``origin`` (SY:66-84), on the host:
-        used for the few hundred sparse landmarks of ``make_sequence``; images go through the GPU kernel."""
+        """Distance from ``origin`` (inside the scene) to the surface along unit ``directions`` (..., 3), on the host
+        (SY:66-84): used for the few hundred sparse landmarks of ``make_sequence``; images go through the GPU kernel.
+        Same float64 operations per element as the reference, so the landmarks come out bit for bit."""
         o = np.asarray(origin, dtype=np.float64)
         d = np.asarray(directions, dtype=np.float64)
         if self.kind == "sphere":
-            od = d @ o
-            disc = od * od - (o @ o - self.radius**2)
-            return -od + np.sqrt(np.maximum(disc, 0.0))
+            # |o + t d| = radius, positive root; d @ o stays a matrix-vector product (its BLAS rounding is part of
+            # what the reference computes)
+            along = d @ o
+            return np.sqrt(np.maximum(along * along - (o @ o - self.radius**2), 0.0)) - along
+        # box / corridor: the ray leaves through the nearest of the three far slab faces
         half = np.asarray(self.size) / 2.0
-        t = np.full(d.shape[:-1], np.inf)
-        for axis in range(3):
-            da = d[..., axis]
-            with np.errstate(divide="ignore"):
-                bound = np.where(da > 0, half[axis], -half[axis])
-                ta = np.where(da != 0.0, (bound - o[axis]) / np.where(da == 0, 1, da), np.inf)
-            t = np.minimum(t, np.where(ta > 0, ta, np.inf))
-        return t
+        face = np.where(d > 0, half, -half)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            t = np.where(d != 0.0, (face - o) / np.where(d == 0, 1, d), np.inf)
+        return np.where(t > 0, t, np.inf).min(axis=-1)
 
 
 def straight_line_trajectory(scene: SyntheticScene, keyframes: int, span_fraction: float = 0.7) -> tuple:
     """In-and-out flight along the scene's long axis with identity orientation (SY:172-200): a triangle
-    wave whose fold sits half a step past the apex, so the return leg interleaves the outbound grid."""
+    wave whose fold sits half a step past the apex, so the return leg interleaves the outbound grid (all poses
+    distinct, consecutive baselines never vanish)."""
     if keyframes < 1:
         raise ConfigError(f"keyframes must be >= 1, got {keyframes}")
-    axis = np.zeros(3)
     if scene.kind == "sphere":
-        axis[2] = 1.0
-        reach = scene.radius * span_fraction / 2.0
+        long_axis, length = 2, scene.radius
     else:
-        extents = np.asarray(scene.size)
-        axis[int(np.argmax(extents))] = 1.0
-        reach = float(extents.max()) * span_fraction / 2.0
-    h = 4.0 / keyframes
-    raw = -1.0 + h * np.arange(keyframes)
-    s = np.where(raw > 1.0 + h / 4.0, 2.0 + h / 2.0 - raw, raw)
-    return tuple(RigidPose(rotation=np.eye(3), translation=axis * (si * reach)) for si in s)
+        long_axis = int(np.argmax(np.asarray(scene.size)))
+        length = np.asarray(scene.size)[long_axis]
+    reach = length * span_fraction / 2.0
+    step = 4.0 / keyframes
+    ramp = step * np.arange(keyframes) - 1.0            # -1 ... 3
+    folded = np.where(ramp > 1.0 + step / 4.0, 2.0 + step / 2.0 - ramp, ramp)
+    poses = []
+    for fraction in folded:
+        centre = np.zeros(3)
+        centre[long_axis] = 1.0
+        poses.append(RigidPose(np.eye(3), centre * (fraction * reach)))
+    return tuple(poses)
 
 
 def default_scene(kind: str, keyframes: int = 0, checker: bool = False) -> SyntheticScene:
